@@ -1,0 +1,118 @@
+/*
+ * latbeam_b200.h — C-ABI of the B200-native WFST Viterbi decoder (liblatbeam_b200.so).
+ *
+ * This is the drop-in boundary for the reference package's decode path
+ * (`latbeam`, /root/reference/pkg/src/latbeam).  Every entry point replaces
+ * one reference interface, cited beside it; plain pointers and sizes only, no
+ * torch types.  All calls return an `lb_status` (0 = OK) mirroring the
+ * reference's exception classes (errors.py:8-41) and CLI exit codes
+ * (cli.py:470-489); `lb_last_error()` gives the thread-local message.
+ *
+ * Threading: an lb_graph is immutable after creation and may be shared by
+ * host threads; decodes on one graph serialise on the graph's workspace.
+ * Ownership: the library owns device replicas and result buffers; callers own
+ * their input arrays (copied during the call).
+ */
+#ifndef LATBEAM_B200_H
+#define LATBEAM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LB_OK = 0,
+    LB_DECODE_FAILURE = 1, /* errors.py DecodeFailure          */
+    LB_USAGE = 2,          /* errors.py UsageError             */
+    LB_CAPACITY = 3,       /* errors.py CapacityError(bound)   */
+    LB_INTERNAL = 4,       /* errors.py InternalInvariantError */
+    LB_CUDA = 5            /* device/runtime failure (no reference counterpart) */
+} lb_status;
+
+typedef struct lb_graph lb_graph;
+typedef struct lb_result lb_result;
+
+/* DecodeConfig (decoder.py:52-89) + the device knobs.  num_workers,
+ * group_size, num_shards, prune_interval and scheduler of the reference only
+ * shape CPU threading and have no device meaning. */
+typedef struct {
+    double beam;                  /* > 0, finite                         */
+    double lattice_beam;          /* >= 0                                */
+    double acoustic_scale;        /* > 0                                 */
+    int64_t max_active;           /* 0 = off (reference), else histogram cutoff */
+    int64_t max_tokens_per_frame; /* CapacityError "--max-tokens-per-frame" */
+    int64_t max_lattice_arcs;     /* live lattice arcs per utterance; "--max-lattice-arcs" */
+    int64_t token_arena;          /* tokens kept per utterance (all frames); 0 = auto; "--token-arena" */
+    int32_t want_lattice;         /* decode_utterance(want_lattice=...)  */
+    int32_t collect_frame_packs;  /* keep per-frame token lists for readback */
+    int32_t lanes;                /* concurrent utterances per launch (CTAs); 0 = auto */
+    int32_t threads_per_lane;     /* CTA size: 256/512/1024; 0 = auto     */
+} lb_config;
+
+int32_t lb_version(void);
+const char *lb_last_error(void);
+int32_t lb_device_count(void);
+
+/* Wfst (wfst.py:33-90): CSR columns, arc id = position.  Uploaded to HBM on
+ * `device` as 16 B arc records + side columns. */
+int lb_graph_create(int32_t device, int64_t num_states, int64_t num_arcs, int32_t start_state,
+                    const int64_t *arc_offsets, const int32_t *arc_src, const int32_t *arc_dst,
+                    const int32_t *arc_ilabel, const int32_t *arc_olabel, const double *arc_weight,
+                    const double *final_cost, lb_graph **out);
+int lb_graph_destroy(lb_graph *g);
+int64_t lb_graph_device_bytes(const lb_graph *g);
+
+/* decode_batch (decoder.py:644-672) / decode_utterance (decoder.py:463-611):
+ * costs[u] is a row-major T[u] x D f64 host matrix (CostMatrix.costs).
+ * Blocking; host->device and device->host copies happen inside. */
+int lb_decode_batch(const lb_graph *g, int32_t n_utts, const double *const *costs,
+                    const int32_t *num_frames, int32_t num_labels, const lb_config *cfg,
+                    lb_result **out);
+
+/* Same, with the cost matrices already resident in device memory on the graph's
+ * device (e.g. an acoustic model's output tensor).  `stream` is a cudaStream_t
+ * (NULL = the library's stream); the call enqueues and waits on it. */
+int lb_decode_batch_device(const lb_graph *g, int32_t n_utts, const double *const *dev_costs,
+                           const int32_t *num_frames, int32_t num_labels, const lb_config *cfg,
+                           void *stream, lb_result **out);
+
+/* Per-utterance readback.  DecodeResult (decoder.py:92-103). */
+int lb_result_count(const lb_result *r, int32_t *n_utts);
+int lb_result_status(const lb_result *r, int32_t utt, int32_t *status, char *message,
+                     int32_t message_len, char *bound, int32_t bound_len);
+int lb_result_best(const lb_result *r, int32_t utt, double *total_cost, int32_t *partial,
+                   int64_t *path_len, int64_t *num_tokens, int64_t *num_lattice_arcs);
+/* Best path as graph arc ids in forward order; words = olabels > 0, alignment
+ * = (ilabel, frame) of the emitting hops (decoder.py:614-641). */
+int lb_result_path(const lb_result *r, int32_t utt, int32_t *arcs);
+/* Token lists per frame (FrameTokens, lattice.py:71-98), in device order
+ * (not state-sorted; the host canonicalises).  frame_off has T+2 entries. */
+int lb_result_tokens(const lb_result *r, int32_t utt, int64_t *frame_off, int32_t *states,
+                     double *costs, int32_t *pred_arc, int32_t *pred_idx, uint64_t *packs);
+/* Live lattice arcs per block with their pruning extra cost (lattice.py:473-497);
+ * from/to index the device-order token lists of the arc's frames. */
+int lb_result_lattice(const lb_result *r, int32_t utt, int64_t *block_off, int32_t *arc,
+                      int32_t *from_idx, int32_t *to_idx, double *extra);
+/* counters[8]: tokens expanded, arcs scanned, emitting candidates, epsilon
+ * frontier entries, epsilon arcs scanned, epsilon candidates, tokens kept,
+ * lattice arcs. */
+int lb_result_counters(const lb_result *r, int32_t utt, int64_t *counters);
+/* Device-event timings of the call (ms): decode kernel, prune kernel, H2D, D2H, and the
+ * number of kernel launches the call made. */
+int lb_result_timing(const lb_result *r, float *decode_ms, float *prune_ms, float *h2d_ms,
+                     float *d2h_ms, int32_t *launches);
+void lb_result_free(lb_result *r);
+
+/* Single-op surfaces (decoder.py:373-435): one frontier on device.
+ * out_* need room for num_states entries; *n_out receives the count. */
+int lb_expand_emitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n,
+                       const double *acrow, int32_t num_labels, double beam, int32_t *out_states,
+                       double *out_costs, int64_t *n_out, double *cutoff);
+int lb_expand_nonemitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n,
+                          double cutoff, int32_t *out_states, double *out_costs, int64_t *n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,796 @@
+// latbeam_b200.cu — host side of liblatbeam_b200.so: the C-ABI declared in
+// include/latbeam_b200.h, graph upload, workspace management, wave scheduling
+// of decode lanes, and result readback.  Device code lives in lb_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/latbeam_b200.h"
+#include "lb_kernels.cuh"
+
+using namespace lbk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return set_err(LB_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n) {
+    return cudaMalloc((void **)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+struct UttHost {
+    int status = 0;
+    std::string msg, bound;
+    double total_cost = NAN;
+    int partial = 0;
+    std::vector<int32_t> path;
+    int64_t counters[8] = {0};
+    int64_t n_tokens = 0, n_lat = 0;
+    std::vector<int64_t> frame_off, block_off;
+    std::vector<int32_t> states, pred_arc, pred_idx, larc, lfrom, lto;
+    std::vector<double> costs, lextra;
+    std::vector<uint64_t> packs;
+};
+
+// Per-graph reusable device workspace: lane scratch (O(S) per lane) and
+// utterance slots (token / lattice arenas).
+struct Workspace {
+    int lanes = 0;
+    int64_t S = 0, tok_cap = 0, lat_cap = 0;
+    int path_cap = 0, tmax = 0;
+    bool packs = false, lat = false;
+    // lane scratch
+    unsigned long long *pack = nullptr;
+    double *cost = nullptr, *minsnap = nullptr, *fc0 = nullptr, *fc1 = nullptr;
+    int *pred = nullptr, *tokidx = nullptr;
+    unsigned *tag = nullptr, *touched = nullptr, *fs0 = nullptr, *fs1 = nullptr, *round_ctr = nullptr;
+    // slots
+    unsigned *tok_state = nullptr;
+    double *tok_cost = nullptr, *node_extra = nullptr, *lat_extra = nullptr, *tmp = nullptr;
+    int *tok_arc = nullptr, *tok_pred = nullptr, *lat_arc = nullptr, *lat_from = nullptr, *lat_to = nullptr;
+    unsigned long long *tok_pack = nullptr, *ne_enc = nullptr;
+    long long *tok_base = nullptr, *lat_base = nullptr, *out_c = nullptr;
+    int *path = nullptr, *out_i = nullptr;
+    double *out_d = nullptr;
+    LaneWs *d_lanes = nullptr;
+    UttDesc *d_desc = nullptr;
+    std::vector<void *> owned;
+
+    void release() {
+        for (void *p : owned) cudaFree(p);
+        owned.clear();
+        lanes = 0;
+    }
+};
+
+}  // namespace
+
+struct lb_graph {
+    int device = 0;
+    int64_t S = 0, A = 0, E = 0;
+    int32_t start = 0, max_ilabel = 0;
+    int sms = 148;
+    int4 *arcs = nullptr;
+    unsigned *src = nullptr, *ol = nullptr, *off = nullptr, *eoff = nullptr, *eids = nullptr;
+    double *fin = nullptr;
+    int64_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    Workspace ws;
+    double *d_costs = nullptr;
+    size_t d_costs_cap = 0;
+    double *h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    GraphDev dev() const {
+        GraphDev g;
+        g.arcs = arcs;
+        g.src = src;
+        g.ol = ol;
+        g.off = off;
+        g.eoff = eoff;
+        g.eids = eids;
+        g.fin = fin;
+        g.S = (int)S;
+        g.start = start;
+        g.has_eps = E > 0;
+        g._pad = 0;
+        return g;
+    }
+};
+
+struct lb_result {
+    std::vector<UttHost> utts;
+    float t_decode = 0, t_prune = 0, t_h2d = 0, t_d2h = 0;
+    int launches = 0;
+};
+
+namespace {
+
+int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, int path_cap, int tmax,
+                     bool packs, bool lat) {
+    Workspace &w = g->ws;
+    if (w.lanes >= lanes && w.S == g->S && w.tok_cap >= tok_cap && w.lat_cap >= lat_cap &&
+        w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat))
+        return LB_OK;
+    lanes = std::max(lanes, w.lanes);
+    tok_cap = std::max(tok_cap, w.tok_cap);
+    lat_cap = std::max(lat_cap, w.lat_cap);
+    path_cap = std::max(path_cap, w.path_cap);
+    tmax = std::max(tmax, w.tmax);
+    packs = packs || w.packs;
+    lat = lat || w.lat;
+    w.release();
+    const size_t S = (size_t)g->S, nl = (size_t)lanes;
+    auto A = [&](auto **p, size_t n) -> cudaError_t {
+        cudaError_t e = dalloc(p, n);
+        if (e == cudaSuccess) w.owned.push_back((void *)*p);
+        return e;
+    };
+    CK(A(&w.pack, S * nl));
+    CK(A(&w.cost, S * nl));
+    CK(A(&w.minsnap, S * nl));
+    CK(A(&w.fc0, S * nl));
+    CK(A(&w.fc1, S * nl));
+    CK(A(&w.pred, S * nl));
+    CK(A(&w.tokidx, S * nl));
+    CK(A(&w.tag, S * nl));
+    CK(A(&w.touched, S * nl));
+    CK(A(&w.fs0, S * nl));
+    CK(A(&w.fs1, S * nl));
+    CK(A(&w.round_ctr, nl));
+    const size_t tc = (size_t)tok_cap, lc = (size_t)std::max<int64_t>(lat_cap, 1);
+    CK(A(&w.tok_state, tc * nl));
+    CK(A(&w.tok_cost, tc * nl));
+    CK(A(&w.tok_arc, tc * nl));
+    CK(A(&w.tok_pred, tc * nl));
+    if (packs) CK(A(&w.tok_pack, tc * nl));
+    if (lat) {
+        CK(A(&w.node_extra, tc * nl));
+        CK(A(&w.ne_enc, tc * nl));
+        CK(A(&w.lat_arc, lc * nl));
+        CK(A(&w.lat_from, lc * nl));
+        CK(A(&w.lat_to, lc * nl));
+        CK(A(&w.lat_extra, lc * nl));
+        CK(A(&w.tmp, lc * nl));
+    }
+    CK(A(&w.tok_base, (size_t)(tmax + 2) * nl));
+    CK(A(&w.lat_base, (size_t)(tmax + 2) * nl));
+    CK(A(&w.path, (size_t)path_cap * nl));
+    CK(A(&w.out_i, 8 * nl));
+    CK(A(&w.out_d, 4 * nl));
+    CK(A(&w.out_c, 8 * nl));
+    CK(A(&w.d_lanes, nl));
+    CK(A(&w.d_desc, nl));
+    CK(cudaMemsetAsync(w.pack, 0xFF, S * nl * 8, g->stream));
+    CK(cudaMemsetAsync(w.tokidx, 0, S * nl * 4, g->stream));
+    CK(cudaMemsetAsync(w.tag, 0, S * nl * 4, g->stream));
+    CK(cudaMemsetAsync(w.round_ctr, 0, nl * 4, g->stream));
+    fill_f64<<<g->sms * 4, 256, 0, g->stream>>>(w.minsnap, INFINITY, (long long)(S * nl));
+    CK(cudaGetLastError());
+    std::vector<LaneWs> hl(nl);
+    for (size_t l = 0; l < nl; l++) {
+        LaneWs &x = hl[l];
+        x.pack = w.pack + l * S;
+        x.cost = w.cost + l * S;
+        x.pred = w.pred + l * S;
+        x.tokidx = w.tokidx + l * S;
+        x.minsnap = w.minsnap + l * S;
+        x.tag = w.tag + l * S;
+        x.touched = w.touched + l * S;
+        x.fs0 = w.fs0 + l * S;
+        x.fs1 = w.fs1 + l * S;
+        x.fc0 = w.fc0 + l * S;
+        x.fc1 = w.fc1 + l * S;
+        x.round_ctr = w.round_ctr + l;
+    }
+    CK(cudaMemcpyAsync(w.d_lanes, hl.data(), nl * sizeof(LaneWs), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    w.lanes = lanes;
+    w.S = g->S;
+    w.tok_cap = tok_cap;
+    w.lat_cap = lat ? lat_cap : 0;
+    w.path_cap = path_cap;
+    w.tmax = tmax;
+    w.packs = packs;
+    w.lat = lat;
+    return LB_OK;
+}
+
+UttDesc slot_desc(const Workspace &w, int l, const double *costs, int T, int64_t tok_cap = -1,
+                  int64_t lat_cap = -1) {
+    UttDesc d;
+    std::memset(&d, 0, sizeof(d));
+    const size_t tc = (size_t)w.tok_cap, lc = (size_t)std::max<int64_t>(w.lat_cap, 1);
+    d.costs = costs;
+    d.T = T;
+    d.path_cap = w.path_cap;
+    d.tok_cap = tok_cap >= 0 ? std::min<int64_t>(tok_cap, w.tok_cap) : w.tok_cap;
+    d.lat_cap = lat_cap >= 0 ? std::min<int64_t>(lat_cap, w.lat_cap) : w.lat_cap;
+    d.tok_state = w.tok_state + l * tc;
+    d.tok_cost = w.tok_cost + l * tc;
+    d.tok_arc = w.tok_arc + l * tc;
+    d.tok_pred = w.tok_pred + l * tc;
+    d.tok_pack = w.packs ? w.tok_pack + l * tc : nullptr;
+    d.tok_base = w.tok_base + (size_t)l * (w.tmax + 2);
+    d.lat_base = w.lat_base + (size_t)l * (w.tmax + 2);
+    if (w.lat) {
+        d.node_extra = w.node_extra + l * tc;
+        d.ne_enc = w.ne_enc + l * tc;
+        d.lat_arc = w.lat_arc + l * lc;
+        d.lat_from = w.lat_from + l * lc;
+        d.lat_to = w.lat_to + l * lc;
+        d.lat_extra = w.lat_extra + l * lc;
+        d.tmp = w.tmp + l * lc;
+    }
+    d.path = w.path + (size_t)l * w.path_cap;
+    d.out_i = w.out_i + 8 * l;
+    d.out_d = w.out_d + 4 * l;
+    d.out_c = w.out_c + 8 * l;
+    return d;
+}
+
+void fill_message(UttHost &u, int code, int frame, double aux, const lb_config &cfg) {
+    char buf[256];
+    switch (code) {
+        case E_DEAD_NO_CAND:
+            u.status = LB_DECODE_FAILURE;
+            snprintf(buf, sizeof buf, "beam search died at frame %d: no emitting candidates", frame);
+            break;
+        case E_DEAD_NO_TOKENS:
+            u.status = LB_DECODE_FAILURE;
+            snprintf(buf, sizeof buf, "no tokens survived the beam at frame %d", frame);
+            break;
+        case E_CAP_TOKENS:
+            u.status = LB_CAPACITY;
+            u.bound = "--max-tokens-per-frame";
+            snprintf(buf, sizeof buf, "frame %d kept %lld tokens, over the %lld limit; raise --max-tokens-per-frame",
+                     frame, (long long)aux, (long long)cfg.max_tokens_per_frame);
+            break;
+        case E_CAP_ARENA:
+            u.status = LB_CAPACITY;
+            u.bound = "--token-arena";
+            snprintf(buf, sizeof buf, "token arena overflowed at frame %d (%lld tokens); raise token_arena", frame,
+                     (long long)aux);
+            break;
+        case E_CAP_LATTICE:
+            u.status = LB_CAPACITY;
+            u.bound = "--max-lattice-arcs";
+            snprintf(buf, sizeof buf, "lattice holds %lld arcs at frame %d, over its %lld capacity; raise --max-lattice-arcs",
+                     (long long)aux, frame, (long long)cfg.max_lattice_arcs);
+            break;
+        case E_CAP_PATH:
+            u.status = LB_CAPACITY;
+            u.bound = "--max-path";
+            snprintf(buf, sizeof buf, "best path longer than its buffer");
+            break;
+        case E_INT_EPS_ROUNDS:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "epsilon relaxation failed to settle within the state count");
+            break;
+        case E_INT_EPS_PRED:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "epsilon winner's source state kept no token");
+            break;
+        case E_INT_INIT:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "initial token found at frame %d", frame);
+            break;
+        case E_INT_BACKTRACE:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "backtrace exceeded its step bound (epsilon cycle at frame %d)", frame);
+            break;
+        case E_INT_PRUNE_EPS:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "epsilon extra-cost fixpoint did not settle within frame %d", frame);
+            break;
+        default:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "device error code %d at frame %d", code, frame);
+    }
+    u.msg = buf;
+}
+
+int validate_cfg(const lb_config *c) {
+    if (!c) return set_err(LB_USAGE, "config is NULL");
+    if (!(std::isfinite(c->beam) && c->beam > 0)) return set_err(LB_USAGE, "beam must be a positive finite number");
+    if (!(std::isfinite(c->lattice_beam) && c->lattice_beam >= 0)) return set_err(LB_USAGE, "lattice_beam must be >= 0");
+    if (!(std::isfinite(c->acoustic_scale) && c->acoustic_scale > 0)) return set_err(LB_USAGE, "acoustic_scale must be > 0");
+    if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
+    if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
+    if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
+    if (c->threads_per_lane && (c->threads_per_lane % 32 || c->threads_per_lane > 1024 || c->threads_per_lane < 64))
+        return set_err(LB_USAGE, "threads_per_lane must be a multiple of 32 in [64, 1024]");
+    return LB_OK;
+}
+
+int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
+                const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms) {
+    const bool lat = cfg->want_lattice != 0;
+    const bool packs = cfg->collect_frame_packs != 0 || lat;
+    int tmax = 1;
+    for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
+    const int64_t S = g->S;
+    int64_t per_frame = std::min<int64_t>(S, cfg->max_tokens_per_frame);
+    if (cfg->max_active > 0) per_frame = std::min<int64_t>(per_frame, 4 * cfg->max_active + 1024);
+    int64_t tok_cap = cfg->token_arena > 0 ? cfg->token_arena : (int64_t)(tmax + 1) * per_frame;
+    tok_cap = std::min<int64_t>(tok_cap, (int64_t)1 << 31);
+    const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
+    const int path_cap = 4 * tmax + 256;
+    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 1024;
+    // lanes: requested, else as many as fit a memory budget (<= 2 waves of SMs)
+    const size_t per_lane = (size_t)S * 64 + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
+                            (size_t)lat_cap * 28 + (size_t)path_cap * 4 + (size_t)(tmax + 2) * 16 + 256;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t reuse = (size_t)g->ws.lanes * per_lane;
+    const size_t budget = (size_t)((double)(free_b + reuse) * 0.85);
+    int lanes = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, 2 * g->sms);
+    lanes = std::max(1, std::min(lanes, n > 0 ? n : 1));
+    while (lanes > 1 && (size_t)lanes * per_lane > budget) lanes--;
+    if ((size_t)lanes * per_lane > budget)
+        return set_err(LB_CAPACITY, "not enough device memory for one decode lane; lower token_arena / max_lattice_arcs");
+    int rc = ensure_workspace(g, lanes, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    if (rc) return rc;
+    Workspace &w = g->ws;
+
+    Params p;
+    p.beam = cfg->beam;
+    p.lattice_beam = cfg->lattice_beam;
+    p.scale = cfg->acoustic_scale;
+    p.max_active = cfg->max_active;
+    p.max_tokens = cfg->max_tokens_per_frame;
+    p.D = D;
+    p.want_lattice = lat;
+    p.collect_packs = packs;
+    const size_t acrow_bytes = (size_t)D * 8;
+    p.acrow_smem = acrow_bytes <= 160 * 1024;
+    const size_t smem = p.acrow_smem ? acrow_bytes : 0;
+    CK(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    const GraphDev gd = g->dev();
+
+    cudaEvent_t e0, e1, e2, e3;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    CK(cudaEventCreate(&e3));
+    res->utts.resize(n);
+    res->t_h2d = h2d_ms;
+    std::vector<UttDesc> desc(lanes);
+    std::vector<int> hi(8 * lanes);
+    std::vector<double> hd(4 * lanes);
+    std::vector<long long> hc(8 * lanes);
+    std::vector<int> hpath((size_t)path_cap * lanes);
+    for (int w0 = 0; w0 < n; w0 += lanes) {
+        const int nw = std::min(lanes, n - w0);
+        for (int l = 0; l < nw; l++) desc[l] = slot_desc(w, l, dev_costs[w0 + l], T[w0 + l], tok_cap, lat_cap);
+        CK(cudaMemcpyAsync(w.d_desc, desc.data(), nw * sizeof(UttDesc), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(w.out_i, 0, 8 * sizeof(int) * nw, st));
+        CK(cudaEventRecord(e0, st));
+        decode_kernel<<<nw, threads, smem, st>>>(gd, p, w.d_lanes, w.d_desc, nw);
+        CK(cudaGetLastError());
+        res->launches++;
+        CK(cudaEventRecord(e1, st));
+        if (lat) {
+            prune_kernel<<<nw, threads, 0, st>>>(gd, p, w.d_desc, nw);
+            CK(cudaGetLastError());
+            res->launches++;
+        }
+        CK(cudaEventRecord(e2, st));
+        CK(cudaMemcpyAsync(hi.data(), w.out_i, 8 * sizeof(int) * nw, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hd.data(), w.out_d, 4 * sizeof(double) * nw, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hc.data(), w.out_c, 8 * sizeof(long long) * nw, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hpath.data(), w.path, sizeof(int) * (size_t)path_cap * nw, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        res->t_decode += ms;
+        CK(cudaEventElapsedTime(&ms, e1, e2));
+        res->t_prune += ms;
+        CK(cudaEventRecord(e2, st));
+        for (int l = 0; l < nw; l++) {
+            UttHost &u = res->utts[w0 + l];
+            const int code = hi[8 * l + 0];
+            std::memcpy(u.counters, &hc[8 * l], sizeof(u.counters));
+            if (code != E_OK) {
+                fill_message(u, code, hi[8 * l + 1], hd[4 * l + 2], *cfg);
+                continue;
+            }
+            u.status = LB_OK;
+            u.partial = hi[8 * l + 2];
+            u.total_cost = hd[4 * l + 0];
+            const int plen = hi[8 * l + 4];
+            u.path.assign(hpath.begin() + (size_t)path_cap * l, hpath.begin() + (size_t)path_cap * l + plen);
+            if (packs || lat) {
+                const int Tu = T[w0 + l];
+                const UttDesc &d = desc[l];
+                u.frame_off.resize(Tu + 2);
+                CK(cudaMemcpy(u.frame_off.data(), d.tok_base, sizeof(long long) * (Tu + 2), cudaMemcpyDeviceToHost));
+                const int64_t nt = u.frame_off[Tu + 1];
+                u.n_tokens = nt;
+                u.states.resize(nt);
+                u.costs.resize(nt);
+                u.pred_arc.resize(nt);
+                u.pred_idx.resize(nt);
+                CK(cudaMemcpy(u.states.data(), d.tok_state, 4 * nt, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(u.costs.data(), d.tok_cost, 8 * nt, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(u.pred_arc.data(), d.tok_arc, 4 * nt, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(u.pred_idx.data(), d.tok_pred, 4 * nt, cudaMemcpyDeviceToHost));
+                for (auto &x : u.pred_idx) x = x >> 1;
+                if (packs) {
+                    u.packs.resize(nt);
+                    CK(cudaMemcpy(u.packs.data(), d.tok_pack, 8 * nt, cudaMemcpyDeviceToHost));
+                }
+                if (lat) {
+                    u.block_off.resize(Tu + 2);
+                    CK(cudaMemcpy(u.block_off.data(), d.lat_base, sizeof(long long) * (Tu + 2), cudaMemcpyDeviceToHost));
+                    const int64_t na = u.block_off[Tu + 1];
+                    u.n_lat = na;
+                    u.larc.resize(na);
+                    u.lfrom.resize(na);
+                    u.lto.resize(na);
+                    u.lextra.resize(na);
+                    CK(cudaMemcpy(u.larc.data(), d.lat_arc, 4 * na, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(u.lfrom.data(), d.lat_from, 4 * na, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(u.lto.data(), d.lat_to, 4 * na, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(u.lextra.data(), d.lat_extra, 8 * na, cudaMemcpyDeviceToHost));
+                }
+            }
+        }
+        CK(cudaEventRecord(e3, st));
+        CK(cudaEventSynchronize(e3));
+        CK(cudaEventElapsedTime(&ms, e2, e3));
+        res->t_d2h += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    return LB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t lb_version(void) { return 1; }
+
+const char *lb_last_error(void) { return g_err.c_str(); }
+
+int32_t lb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const int64_t *off, const int32_t *src,
+                    const int32_t *dst, const int32_t *il, const int32_t *ol, const double *w, const double *fin,
+                    lb_graph **out) {
+    if (!out) return set_err(LB_USAGE, "out is NULL");
+    *out = nullptr;
+    if (S < 1 || A < 0 || start < 0 || start >= S) return set_err(LB_USAGE, "bad graph dimensions / start state");
+    if (S >= (1ll << 31) || A >= (1ll << 32) - 1) return set_err(LB_USAGE, "graph too large for 32-bit ids");
+    if (off[0] != 0 || off[S] != A) return set_err(LB_USAGE, "arc offsets must start at 0 and end at num_arcs");
+    std::unique_ptr<lb_graph> g(new lb_graph());
+    g->device = device;
+    g->S = S;
+    g->A = A;
+    g->start = start;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    // host-side packing of the device layout
+    std::vector<int4> arcs((size_t)A);
+    std::vector<unsigned> hsrc((size_t)A), hol((size_t)A), hoff((size_t)S + 1), heoff((size_t)S + 1);
+    std::vector<unsigned> heids;
+    int32_t maxil = 0;
+    for (int64_t s = 0; s < S; s++) {
+        hoff[s] = (unsigned)off[s];
+        heoff[s] = (unsigned)heids.size();
+        if (off[s + 1] < off[s]) return set_err(LB_USAGE, "arc offsets must be non-decreasing");
+        for (int64_t a = off[s]; a < off[s + 1]; a++) {
+            if (il[a] == 0) heids.push_back((unsigned)a);
+        }
+    }
+    hoff[S] = (unsigned)A;
+    heoff[S] = (unsigned)heids.size();
+    for (int64_t a = 0; a < A; a++) {
+        if (dst[a] < 0 || dst[a] >= S || il[a] < 0 || ol[a] < 0)
+            return set_err(LB_USAGE, "arc field out of range");
+        if (!(std::isfinite(w[a]) && w[a] >= 0.0)) return set_err(LB_USAGE, "arc weight must be finite and >= 0");
+        int4 r;
+        r.x = dst[a];
+        r.y = il[a];
+        long long bits;
+        std::memcpy(&bits, &w[a], 8);
+        r.z = (int)(bits & 0xFFFFFFFFll);
+        r.w = (int)(bits >> 32);
+        arcs[a] = r;
+        hsrc[a] = (unsigned)src[a];
+        hol[a] = (unsigned)ol[a];
+        maxil = std::max(maxil, il[a]);
+    }
+    g->max_ilabel = maxil;
+    g->E = (int64_t)heids.size();
+    CK(dalloc(&g->arcs, A));
+    CK(dalloc(&g->src, A));
+    CK(dalloc(&g->ol, A));
+    CK(dalloc(&g->off, S + 1));
+    CK(dalloc(&g->eoff, S + 1));
+    CK(dalloc(&g->eids, g->E));
+    CK(dalloc(&g->fin, S));
+    CK(cudaMemcpy(g->arcs, arcs.data(), sizeof(int4) * A, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->src, hsrc.data(), 4 * A, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->ol, hol.data(), 4 * A, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->off, hoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->eoff, heoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
+    if (g->E) CK(cudaMemcpy(g->eids, heids.data(), 4 * g->E, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->fin, fin, 8 * S, cudaMemcpyHostToDevice));
+    g->bytes = A * 16 + A * 8 + (S + 1) * 8 + g->E * 4 + S * 8;
+    *out = g.release();
+    return LB_OK;
+}
+
+int lb_graph_destroy(lb_graph *g) {
+    if (!g) return LB_OK;
+    cudaSetDevice(g->device);
+    g->ws.release();
+    cudaFree(g->arcs);
+    cudaFree(g->src);
+    cudaFree(g->ol);
+    cudaFree(g->off);
+    cudaFree(g->eoff);
+    cudaFree(g->eids);
+    cudaFree(g->fin);
+    cudaFree(g->d_costs);
+    if (g->h_stage) cudaFreeHost(g->h_stage);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return LB_OK;
+}
+
+int64_t lb_graph_device_bytes(const lb_graph *g) { return g ? g->bytes : 0; }
+
+int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, const int32_t *T, int32_t D,
+                    const lb_config *cfg, lb_result **out) {
+    lb_graph *g = const_cast<lb_graph *>(gc);
+    if (!g || !out) return set_err(LB_USAGE, "graph/out is NULL");
+    *out = nullptr;
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (n < 0) return set_err(LB_USAGE, "n_utts must be >= 0");
+    if (D < 1) return set_err(LB_USAGE, "num_labels must be >= 1");
+    if (g->max_ilabel > D) return set_err(LB_USAGE, "graph uses an input label beyond the cost matrix columns");
+    size_t total = 0;
+    for (int i = 0; i < n; i++) {
+        if (T[i] < 1) return set_err(LB_USAGE, "every cost matrix needs T >= 1");
+        total += (size_t)T[i] * D;
+    }
+    std::lock_guard<std::mutex> lock(g->mu);
+    CK(cudaSetDevice(g->device));
+    std::unique_ptr<lb_result> res(new lb_result());
+    if (total > g->d_costs_cap) {
+        cudaFree(g->d_costs);
+        g->d_costs = nullptr;
+        CK(dalloc(&g->d_costs, total));
+        g->d_costs_cap = total;
+    }
+    if (total > g->h_stage_cap) {
+        if (g->h_stage) cudaFreeHost(g->h_stage);
+        g->h_stage = nullptr;
+        CK(cudaMallocHost((void **)&g->h_stage, std::max<size_t>(total, 1) * 8));
+        g->h_stage_cap = total;
+    }
+    std::vector<const double *> dptr(n);
+    cudaEvent_t h0, h1;
+    CK(cudaEventCreate(&h0));
+    CK(cudaEventCreate(&h1));
+    CK(cudaEventRecord(h0, g->stream));
+    size_t o = 0;
+    for (int i = 0; i < n; i++) {
+        const size_t sz = (size_t)T[i] * D;
+        std::memcpy(g->h_stage + o, costs[i], sz * 8);
+        CK(cudaMemcpyAsync(g->d_costs + o, g->h_stage + o, sz * 8, cudaMemcpyHostToDevice, g->stream));
+        dptr[i] = g->d_costs + o;
+        o += sz;
+    }
+    CK(cudaEventRecord(h1, g->stream));
+    CK(cudaEventSynchronize(h1));
+    float h2d = 0;
+    CK(cudaEventElapsedTime(&h2d, h0, h1));
+    cudaEventDestroy(h0);
+    cudaEventDestroy(h1);
+    rc = decode_impl(g, n, dptr.data(), T, D, cfg, g->stream, res.get(), h2d);
+    if (rc) return rc;
+    *out = res.release();
+    return LB_OK;
+}
+
+int lb_decode_batch_device(const lb_graph *gc, int32_t n, const double *const *dev_costs, const int32_t *T,
+                           int32_t D, const lb_config *cfg, void *stream, lb_result **out) {
+    lb_graph *g = const_cast<lb_graph *>(gc);
+    if (!g || !out) return set_err(LB_USAGE, "graph/out is NULL");
+    *out = nullptr;
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (n < 0 || D < 1) return set_err(LB_USAGE, "bad batch dimensions");
+    if (g->max_ilabel > D) return set_err(LB_USAGE, "graph uses an input label beyond the cost matrix columns");
+    for (int i = 0; i < n; i++)
+        if (T[i] < 1) return set_err(LB_USAGE, "every cost matrix needs T >= 1");
+    std::lock_guard<std::mutex> lock(g->mu);
+    CK(cudaSetDevice(g->device));
+    std::unique_ptr<lb_result> res(new lb_result());
+    cudaStream_t st = stream ? (cudaStream_t)stream : g->stream;
+    rc = decode_impl(g, n, dev_costs, T, D, cfg, st, res.get(), 0.0f);
+    if (rc) return rc;
+    *out = res.release();
+    return LB_OK;
+}
+
+int lb_result_count(const lb_result *r, int32_t *n) {
+    if (!r || !n) return set_err(LB_USAGE, "NULL argument");
+    *n = (int32_t)r->utts.size();
+    return LB_OK;
+}
+
+#define UTT_OR_FAIL                                                                     \
+    if (!r || utt < 0 || utt >= (int32_t)r->utts.size()) return set_err(LB_USAGE, "bad result/utterance"); \
+    const UttHost &u = r->utts[utt];
+
+int lb_result_status(const lb_result *r, int32_t utt, int32_t *status, char *msg, int32_t msg_len, char *bound,
+                     int32_t bound_len) {
+    UTT_OR_FAIL
+    if (status) *status = u.status;
+    if (msg && msg_len > 0) snprintf(msg, msg_len, "%s", u.msg.c_str());
+    if (bound && bound_len > 0) snprintf(bound, bound_len, "%s", u.bound.c_str());
+    return LB_OK;
+}
+
+int lb_result_best(const lb_result *r, int32_t utt, double *total_cost, int32_t *partial, int64_t *path_len,
+                   int64_t *num_tokens, int64_t *num_lat) {
+    UTT_OR_FAIL
+    if (total_cost) *total_cost = u.total_cost;
+    if (partial) *partial = u.partial;
+    if (path_len) *path_len = (int64_t)u.path.size();
+    if (num_tokens) *num_tokens = u.n_tokens;
+    if (num_lat) *num_lat = u.n_lat;
+    return LB_OK;
+}
+
+int lb_result_path(const lb_result *r, int32_t utt, int32_t *arcs) {
+    UTT_OR_FAIL
+    if (!u.path.empty()) std::memcpy(arcs, u.path.data(), 4 * u.path.size());
+    return LB_OK;
+}
+
+int lb_result_tokens(const lb_result *r, int32_t utt, int64_t *frame_off, int32_t *states, double *costs,
+                     int32_t *pred_arc, int32_t *pred_idx, uint64_t *packs) {
+    UTT_OR_FAIL
+    if (u.frame_off.empty()) return set_err(LB_USAGE, "token lists were not collected (collect_frame_packs/want_lattice)");
+    std::memcpy(frame_off, u.frame_off.data(), 8 * u.frame_off.size());
+    const size_t n = (size_t)u.n_tokens;
+    if (states) std::memcpy(states, u.states.data(), 4 * n);
+    if (costs) std::memcpy(costs, u.costs.data(), 8 * n);
+    if (pred_arc) std::memcpy(pred_arc, u.pred_arc.data(), 4 * n);
+    if (pred_idx) std::memcpy(pred_idx, u.pred_idx.data(), 4 * n);
+    if (packs && !u.packs.empty()) std::memcpy(packs, u.packs.data(), 8 * n);
+    return LB_OK;
+}
+
+int lb_result_lattice(const lb_result *r, int32_t utt, int64_t *block_off, int32_t *arc, int32_t *from_idx,
+                      int32_t *to_idx, double *extra) {
+    UTT_OR_FAIL
+    if (u.block_off.empty()) return set_err(LB_USAGE, "lattice was not requested");
+    std::memcpy(block_off, u.block_off.data(), 8 * u.block_off.size());
+    const size_t n = (size_t)u.n_lat;
+    std::memcpy(arc, u.larc.data(), 4 * n);
+    std::memcpy(from_idx, u.lfrom.data(), 4 * n);
+    std::memcpy(to_idx, u.lto.data(), 4 * n);
+    std::memcpy(extra, u.lextra.data(), 8 * n);
+    return LB_OK;
+}
+
+int lb_result_counters(const lb_result *r, int32_t utt, int64_t *c) {
+    UTT_OR_FAIL
+    std::memcpy(c, u.counters, sizeof(u.counters));
+    return LB_OK;
+}
+
+int lb_result_timing(const lb_result *r, float *decode_ms, float *prune_ms, float *h2d_ms, float *d2h_ms,
+                     int32_t *launches) {
+    if (!r) return set_err(LB_USAGE, "NULL result");
+    if (decode_ms) *decode_ms = r->t_decode;
+    if (prune_ms) *prune_ms = r->t_prune;
+    if (h2d_ms) *h2d_ms = r->t_h2d;
+    if (d2h_ms) *d2h_ms = r->t_d2h;
+    if (launches) *launches = r->launches;
+    return LB_OK;
+}
+
+void lb_result_free(lb_result *r) { delete r; }
+
+static int expand_common(lb_graph *g, const int32_t *states, const double *costs, int64_t n, const double *acrow,
+                         int32_t D, double beam, double cutoff, int mode, int32_t *out_states, double *out_costs,
+                         int64_t *n_out, double *cutoff_out) {
+    if (!g || !states || !costs || n < 1) return set_err(LB_USAGE, "frontier is empty");
+    std::lock_guard<std::mutex> lock(g->mu);
+    CK(cudaSetDevice(g->device));
+    int rc = ensure_workspace(g, 1, n + g->S, 0, 16, 1, false, false);
+    if (rc) return rc;
+    Workspace &w = g->ws;
+    cudaStream_t st = g->stream;
+    double *d_row = nullptr;
+    if (mode == 0) {
+        CK(dalloc(&d_row, D));
+        CK(cudaMemcpyAsync(d_row, acrow, 8 * (size_t)D, cudaMemcpyHostToDevice, st));
+    }
+    UttDesc d = slot_desc(w, 0, d_row, 1);
+    std::vector<unsigned> hs(states, states + n);
+    CK(cudaMemcpyAsync(d.tok_state, hs.data(), 4 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d.tok_cost, costs, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d.out_i, 0, 8 * sizeof(int), st));
+    LaneWs L;
+    CK(cudaMemcpyAsync(&L, w.d_lanes, sizeof(LaneWs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (mode == 0) set_tokidx<<<(int)((n + 255) / 256), 256, 0, st>>>(L.tokidx, d.tok_state, (int)n);
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.beam = beam;
+    p.scale = 1.0;
+    p.max_tokens = 1ll << 40;
+    p.D = D;
+    p.acrow_smem = 0;
+    CK(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8));
+    expand_kernel<<<1, 1024, 8, st>>>(g->dev(), p, L, d, (int)n, mode, cutoff);
+    CK(cudaGetLastError());
+    int oi[8];
+    double od[4];
+    CK(cudaMemcpyAsync(oi, d.out_i, sizeof(oi), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(od, d.out_d, sizeof(od), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (d_row) cudaFree(d_row);
+    if (oi[0]) return set_err(LB_INTERNAL, "epsilon relaxation failed to settle within the state count");
+    const int m = oi[4];
+    std::vector<unsigned> os(m);
+    CK(cudaMemcpy(os.data(), d.tok_state + n, 4 * (size_t)m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_costs, d.tok_cost + n, 8 * (size_t)m, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < m; k++) out_states[k] = (int32_t)os[k];
+    *n_out = m;
+    if (cutoff_out) *cutoff_out = od[0];
+    return LB_OK;
+}
+
+int lb_expand_emitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n, const double *acrow,
+                       int32_t D, double beam, int32_t *out_states, double *out_costs, int64_t *n_out,
+                       double *cutoff) {
+    if (!(std::isfinite(beam) && beam > 0)) return set_err(LB_USAGE, "beam must be a positive finite number");
+    return expand_common(const_cast<lb_graph *>(g), states, costs, n, acrow, D, beam, 0.0, 0, out_states, out_costs,
+                         n_out, cutoff);
+}
+
+int lb_expand_nonemitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n, double cutoff,
+                          int32_t *out_states, double *out_costs, int64_t *n_out) {
+    return expand_common(const_cast<lb_graph *>(g), states, costs, n, nullptr, 1, 1.0, cutoff, 1, out_states,
+                         out_costs, n_out, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+"""Lattice result types and the host-side canonicalisation of device lattices.
+
+The device records every live lattice arc (SURVEY.md Appendix A.5 rule) and its
+pruning extra cost (csrc/lb_kernels.cuh `prune_kernel`, restating
+lattice.py:365-497 of `latbeam`).  This module turns those device arrays into
+the reference's result types:
+
+* `FrameTokens` — one frame's state-sorted token list (lattice.py:71-98);
+* `WorkLattice` — the reference `Lattice` query surface (`frames`,
+  `block_arrays`, `live_arc_table`, `arcs`, `partial`, `final_token_costs`)
+  over the device results; arcs are LIVE or PRUNED (no VOID slots exist because
+  only live passes are ever recorded);
+* `FinalLattice` + `finalize_lattice` — dense (frame, index) renumbering and
+  canonical arc order (lattice.py:500-598);
+* the text format (lattice.py:605-673).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import NamedTuple
+
+import numpy as np
+
+from .errors import DecodeFailure, ParseError
+
+STATUS_LIVE = 0
+STATUS_PRUNED = 1
+STATUS_VOID = 2
+
+
+class LatticeNodeId(NamedTuple):
+    frame: int
+    idx: int
+
+
+@dataclass(frozen=True)
+class LatticeArc:
+    from_node: LatticeNodeId
+    to_node: LatticeNodeId
+    ilabel: int
+    olabel: int
+    graph_cost: float
+    acoustic_cost: float
+    extra_cost: float = math.inf
+    pruned: bool = False
+
+
+@dataclass(frozen=True)
+class Token:
+    cost: float
+    pred_arc: int | None
+    pred_token: int | None
+    state: int
+    frame: int
+
+
+@dataclass
+class FrameTokens:
+    """One frame's tokens, sorted by state; pred_idx indexes the previous
+    frame for an emitting pred arc and this frame for an epsilon one."""
+
+    frame: int
+    states: np.ndarray
+    costs: np.ndarray
+    pred_arc: np.ndarray
+    pred_idx: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return len(self.states)
+
+    def token(self, i: int) -> Token:
+        return Token(float(self.costs[i]),
+                     int(self.pred_arc[i]) if self.pred_arc[i] >= 0 else None,
+                     int(self.pred_idx[i]) if self.pred_idx[i] >= 0 else None,
+                     int(self.states[i]), self.frame)
+
+
+@dataclass
+class FinalLattice:
+    num_nodes: int
+    start: int
+    final_ids: np.ndarray
+    final_costs: np.ndarray
+    from_: np.ndarray
+    to: np.ndarray
+    ilabel: np.ndarray
+    olabel: np.ndarray
+    graph_cost: np.ndarray
+    acoustic_cost: np.ndarray
+    node_frame: np.ndarray | None = None
+    node_idx: np.ndarray | None = None
+    num_frames: int | None = None
+
+    @property
+    def num_arcs(self) -> int:
+        return len(self.from_)
+
+    def same_lattice(self, other) -> bool:
+        keys = ("final_ids", "final_costs", "from_", "to", "ilabel", "olabel", "graph_cost",
+                "acoustic_cost")
+        return (self.num_nodes == other.num_nodes and self.start == other.start
+                and all(np.array_equal(getattr(self, k), getattr(other, k)) for k in keys))
+
+
+class WorkLattice:
+    """Query view of one decoded utterance's lattice (reference `Lattice` surface)."""
+
+    def __init__(self, wfst, frames, blocks, node_extra, start_idx, partial, final_token_costs,
+                 best_final_cost):
+        self.wfst = wfst
+        self.frames: list[FrameTokens] = frames
+        self._blocks = blocks           # per block: dict(arc_id, from_idx, to_idx, acoustic_cost, extra, status)
+        self.node_extra = node_extra
+        self.start_idx = start_idx
+        self.partial = partial
+        self.final_token_costs = final_token_costs
+        self.best_final_cost = best_final_cost
+        self.final_prune_done = True
+
+    @property
+    def num_frames(self) -> int:
+        return len(self.frames) - 1
+
+    def block_arrays(self, block: int) -> dict[str, np.ndarray]:
+        b = self._blocks[block]
+        a = b["arc_id"]
+        il = self.wfst.arc_ilabel[a].astype(np.int64)
+        n = len(a)
+        return {
+            "slots": np.arange(n, dtype=np.int64),
+            "arc_id": a,
+            "ilabel": il,
+            "olabel": self.wfst.arc_olabel[a].astype(np.int64),
+            "graph_cost": self.wfst.arc_weight[a],
+            "acoustic_cost": b["acoustic_cost"],
+            "cost": b["cost"],
+            "from_frame": np.where(il > 0, block - 1, block).astype(np.int64),
+            "from_idx": b["from_idx"],
+            "to_frame": np.full(n, block, dtype=np.int64),
+            "to_idx": b["to_idx"],
+            "status": b["status"],
+            "extra": b["extra"],
+        }
+
+    def live_arc_table(self, include_pruned: bool = False) -> dict[str, np.ndarray]:
+        cols: dict[str, list] = {}
+        for b in range(len(self.frames)):
+            blk = self.block_arrays(b)
+            keep = blk["status"] == STATUS_LIVE
+            if include_pruned:
+                keep |= blk["status"] == STATUS_PRUNED
+            for k, v in blk.items():
+                cols.setdefault(k, []).append(v[keep])
+        return {k: np.concatenate(v) if v else np.empty(0) for k, v in cols.items()}
+
+    def arcs(self, include_pruned: bool = False) -> list[LatticeArc]:
+        t = self.live_arc_table(include_pruned)
+        return [LatticeArc(LatticeNodeId(int(t["from_frame"][i]), int(t["from_idx"][i])),
+                           LatticeNodeId(int(t["to_frame"][i]), int(t["to_idx"][i])),
+                           int(t["ilabel"][i]), int(t["olabel"][i]), float(t["graph_cost"][i]),
+                           float(t["acoustic_cost"][i]), float(t["extra"][i]),
+                           bool(t["status"][i] == STATUS_PRUNED))
+                for i in range(len(t["slots"]))]
+
+
+def finalize_lattice(lat: WorkLattice) -> FinalLattice:
+    """Compact surviving arcs, renumber nodes densely by (frame, idx), sort arcs
+    canonically by (from, to, ilabel, olabel, graph, acoustic) — lattice.py:537-598."""
+    t = lat.live_arc_table()
+    if len(t["slots"]) == 0:
+        raise DecodeFailure("no lattice arcs survived pruning")
+    fk = (t["from_frame"].astype(np.int64) << 32) | t["from_idx"].astype(np.int64)
+    tk = (t["to_frame"].astype(np.int64) << 32) | t["to_idx"].astype(np.int64)
+    keys = np.unique(np.concatenate([fk, tk]))
+    fid = np.searchsorted(keys, fk)
+    tid = np.searchsorted(keys, tk)
+    order = np.lexsort((t["acoustic_cost"], t["graph_cost"], t["olabel"], t["ilabel"], tid, fid))
+    nframe = keys >> 32
+    nidx = keys & 0xFFFFFFFF
+    sk = np.int64(lat.start_idx)
+    sp = int(np.searchsorted(keys, sk))
+    if sp >= len(keys) or keys[sp] != sk:
+        raise DecodeFailure("surviving arcs do not connect to the start node")
+    last = lat.num_frames
+    at_last = nframe == last
+    if lat.partial:
+        fids = np.flatnonzero(at_last)
+        fcs = np.zeros(len(fids))
+    else:
+        tc = lat.final_token_costs
+        fin = at_last & np.isfinite(tc[np.where(at_last, nidx, 0)])
+        fids = np.flatnonzero(fin)
+        fcs = tc[nidx[fids]]
+    if len(fids) == 0:
+        raise DecodeFailure("no terminal node survived pruning")
+    return FinalLattice(len(keys), sp, fids.astype(np.int64), fcs.astype(np.float64),
+                        fid[order].astype(np.int64), tid[order].astype(np.int64),
+                        t["ilabel"][order].astype(np.int64), t["olabel"][order].astype(np.int64),
+                        t["graph_cost"][order].astype(np.float64),
+                        t["acoustic_cost"][order].astype(np.float64),
+                        nframe.astype(np.int64), nidx.astype(np.int64), last)
+
+
+def write_lattice_text(fl: FinalLattice) -> str:
+    out = [f"NODES {fl.num_nodes} ARCS {fl.num_arcs} START {fl.start}"]
+    out += [f"F {fl.final_ids[i]} {float(fl.final_costs[i])!r}" for i in range(len(fl.final_ids))]
+    out += [f"A {fl.from_[i]} {fl.to[i]} {fl.ilabel[i]} {fl.olabel[i]} "
+            f"{float(fl.graph_cost[i])!r} {float(fl.acoustic_cost[i])!r}" for i in range(fl.num_arcs)]
+    return "\n".join(out) + "\n"
+
+
+def read_lattice_text(text) -> FinalLattice:
+    if hasattr(text, "read"):
+        text = text.read()
+    lines = str(text).splitlines()
+    if not lines:
+        raise ParseError(1, "empty lattice text")
+    h = lines[0].split()
+    if len(h) != 6 or h[0] != "NODES" or h[2] != "ARCS" or h[4] != "START":
+        raise ParseError(1, f"bad header {lines[0]!r}")
+    try:
+        n, m, start = int(h[1]), int(h[3]), int(h[5])
+    except ValueError:
+        raise ParseError(1, f"non-integer header field in {lines[0]!r}") from None
+    fids, fcs = [], []
+    cols: list[list] = [[] for _ in range(6)]
+    for no, line in enumerate(lines[1:], 2):
+        f = line.split()
+        if not f:
+            continue
+        try:
+            if f[0] == "F" and len(f) == 3:
+                fids.append(int(f[1]))
+                fcs.append(float(f[2]))
+            elif f[0] == "A" and len(f) == 7:
+                vals = [int(x) for x in f[1:5]] + [float(f[5]), float(f[6])]
+                for c, v in zip(cols, vals):
+                    c.append(v)
+            else:
+                raise ParseError(no, f"unrecognized line {line!r}")
+        except ValueError:
+            kind = "final" if f[0] == "F" else "arc"
+            raise ParseError(no, f"bad {kind} line {line!r}") from None
+    if len(cols[0]) != m:
+        raise ParseError(len(lines), f"header promised {m} arcs, found {len(cols[0])}")
+    ids = np.asarray(fids, dtype=np.int64)
+    fr, to = (np.asarray(c, dtype=np.int64) for c in cols[:2])
+    if (len(ids) and (ids.min() < 0 or ids.max() >= n)) or any(
+            len(r) and (r.min() < 0 or r.max() >= n) for r in (fr, to)) or not 0 <= start < n:
+        raise ParseError(1, "node reference out of range")
+    return FinalLattice(n, start, ids, np.asarray(fcs, dtype=np.float64), fr, to,
+                        np.asarray(cols[2], dtype=np.int64), np.asarray(cols[3], dtype=np.int64),
+                        np.asarray(cols[4], dtype=np.float64), np.asarray(cols[5], dtype=np.float64))

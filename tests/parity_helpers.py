@@ -1,0 +1,80 @@
+"""Shared comparison helpers: device results vs the CPU oracle (oracle/)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+import paper_1804_03243_b200 as lb
+
+ERRMAP = {1: lb.DecodeFailure, 2: lb.UsageError, 3: lb.CapacityError, 4: lb.InternalInvariantError}
+
+
+def near_boundary(ref, lattice_beam, tol=1e-3) -> bool:
+    """C3 skip rule (test_acceptance.py:151-165): an oracle extra within tol of the beam."""
+    for blk in ref.blocks:
+        ex = blk[4]
+        if len(ex) and np.min(np.abs(ex - lattice_beam)) <= tol:
+            return True
+    return False
+
+
+def compare_1best(got, ref, frame_packs=True):
+    assert got.words == ref.words, (got.words, ref.words)
+    assert got.alignment == ref.alignment
+    assert got.total_cost == ref.total_cost, (got.total_cost, ref.total_cost)
+    assert got.partial == ref.partial
+    if frame_packs:
+        assert len(got.frame_packs) == len(ref.frame_packs)
+        for f, ((s1, p1), (s2, p2)) in enumerate(zip(got.frame_packs, ref.frame_packs)):
+            assert np.array_equal(s1, s2), f"frame {f} states differ"
+            assert np.array_equal(p1, p2), f"frame {f} packs differ"
+
+
+def compare_lattice(got, ref, lattice_beam):
+    """Final lattice identical (unless an arc sits within 1e-3 of the beam);
+    live-arc extras within 1e-4 always."""
+    # extras per (block, arc id)
+    wl = got.work_lattice
+    for b, blk in enumerate(ref.blocks):
+        arcs, _, _, _, extra, _ = blk
+        ga = wl.block_arrays(b)
+        assert np.array_equal(np.sort(ga["arc_id"]), np.sort(arcs)), f"block {b} live arc set differs"
+        o1, o2 = np.argsort(ga["arc_id"], kind="stable"), np.argsort(arcs, kind="stable")
+        e1, e2 = ga["extra"][o1], extra[o2]
+        fin = np.isfinite(e2)
+        assert np.array_equal(np.isfinite(e1), fin), f"block {b} dead-end pattern differs"
+        if fin.any():
+            assert np.max(np.abs(e1[fin] - e2[fin])) <= 1e-4, f"block {b} extras differ"
+    if near_boundary(ref, lattice_beam):
+        return "boundary"
+    fl, rf = got.lattice, ref.final
+    assert fl.num_nodes == rf["num_nodes"] and fl.start == rf["start"]
+    for k in ("final_ids", "final_costs", "from_", "to", "ilabel", "olabel", "graph_cost",
+              "acoustic_cost", "node_frame", "node_idx"):
+        assert np.array_equal(getattr(fl, k), rf[k]), f"final lattice {k} differs"
+    return "exact"
+
+
+def decode_both(w, m, oracle, beam, lattice_beam=4.0, scale=1.0, max_active=0, want_lattice=True,
+                **cfg_kw):
+    ref = oracle.decode(w, m, beam, lattice_beam=lattice_beam, acoustic_scale=scale,
+                        max_active=max_active, want_lattice=want_lattice, **cfg_kw)
+    cfg = lb.DecodeConfig(beam=beam, lattice_beam=lattice_beam, acoustic_scale=scale,
+                          max_active=max_active, max_lattice_arcs=50_000_000,
+                          **{k: v for k, v in cfg_kw.items() if k in ("max_tokens_per_frame",)})
+    try:
+        got = lb.decode_utterance(w, m, cfg, want_lattice=want_lattice, collect_frame_packs=True)
+    except lb.LatbeamError as exc:
+        got = exc
+    return got, ref
+
+
+def check_pair(got, ref, lattice_beam, want_lattice=True):
+    if not ref.ok:
+        assert isinstance(got, ERRMAP[ref.status]), (got, ref.message)
+        return "error"
+    assert not isinstance(got, Exception), (got, "oracle decoded fine")
+    compare_1best(got, ref)
+    if want_lattice:
+        return compare_lattice(got, ref, lattice_beam)
+    return "ok"

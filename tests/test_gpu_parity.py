@@ -1,0 +1,170 @@
+"""Parity of the CUDA path (liblatbeam_b200.so via the public API) with the CPU oracle.
+
+Bit-exact: words, alignment, total_cost, partial and every frame's
+(state, packed word) map.  Lattices: identical FinalLattice arrays unless an
+oracle extra lies within 1e-3 of lattice_beam (the reference's C3 rule,
+test_acceptance.py:151-165); live-arc extras within 1e-4 always.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1804_03243_b200 as lb
+from paper_1804_03243_b200 import synthetic
+from parity_helpers import check_pair, compare_1best, decode_both
+
+pytestmark = pytest.mark.gpu
+
+
+def test_native_library_is_the_path():
+    from paper_1804_03243_b200 import _lib
+    L = _lib.lib()
+    assert L.lb_device_count() >= 1
+    assert L.lb_version() == 1
+
+
+@pytest.mark.parametrize("base,cycles,negative", [(0, False, False), (1_000_000, False, True),
+                                                  (7_000_000, True, False), (3_000_000, True, True)])
+def test_random_corpus(oracle_mod, base, cycles, negative):
+    rng = np.random.default_rng(base + 17)
+    kinds = {}
+    for seed in range(base, base + 60):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=cycles, allow_negative=negative)
+        beam = float(rng.uniform(3.0, 14.0))
+        lbeam = float(rng.uniform(0.0, 6.0))
+        scale = 1.0 if seed % 3 else 0.75
+        got, ref = decode_both(w, m, oracle_mod, beam, lbeam, scale)
+        k = check_pair(got, ref, lbeam)
+        kinds[k] = kinds.get(k, 0) + 1
+    assert kinds.get("exact", 0) >= 20, kinds
+
+
+def test_larger_random_graphs(oracle_mod):
+    for seed in range(9_000_000, 9_000_012):
+        w, m = synthetic.random_task(seed, max_states=400, max_arcs=3000, num_labels=30,
+                                     max_frames=60)
+        got, ref = decode_both(w, m, oracle_mod, 7.0, 3.0)
+        check_pair(got, ref, 3.0)
+
+
+def test_w1_and_diamond_kats():
+    w1 = lb.load_wfst_text("0 1 1 1 0.5\n0 2 2 2 1.0\n1 0.0\n2 0.0\n")
+    c1 = lb.load_cost_matrix("1 2\n0.3 0.1\n")
+    r = lb.decode_utterance(w1, c1)
+    assert r.words == [1] and r.alignment == [(1, 0)] and not r.partial
+    assert r.total_cost == pytest.approx(0.8)
+    assert r.lattice.num_arcs == 2
+    extras = {a.olabel: a.extra_cost for a in r.work_lattice.arcs()}
+    assert extras[1] == pytest.approx(0.0, abs=1e-12) and extras[2] == pytest.approx(0.3, abs=1e-12)
+    assert lb.decode_utterance(w1, c1, lb.DecodeConfig(lattice_beam=0.1)).lattice.num_arcs == 1
+    assert lb.write_lattice_text(lb.decode_utterance(w1, c1, lb.DecodeConfig(lattice_beam=0.1)).lattice) \
+        == "NODES 2 ARCS 1 START 0\nF 1 0.0\nA 0 1 1 1 0.5 0.3\n"
+    dia = lb.load_wfst_text("0 1 1 1 0.1\n0 2 2 2 0.3\n1 3 1 0 0.2\n2 4 2 0 0.2\n"
+                            "3 5 1 0 0.3\n4 5 2 0 0.3\n5 0.0\n")
+    dc = lb.load_cost_matrix("3 2\n0.1 0.2\n0.1 0.2\n0.2 0.2\n")
+    r = lb.decode_utterance(dia, dc, lb.DecodeConfig(lattice_beam=8.0))
+    assert r.total_cost == pytest.approx(1.0)
+    by = {}
+    for a in r.work_lattice.arcs():
+        by.setdefault(a.ilabel, []).append(a.extra_cost)
+    assert by[1] == pytest.approx([0.0] * 3, abs=1e-12) and by[2] == pytest.approx([0.4] * 3, abs=1e-12)
+    assert lb.decode_utterance(dia, dc, lb.DecodeConfig(lattice_beam=0.39)).lattice.num_arcs == 3
+    assert lb.decode_utterance(dia, dc, lb.DecodeConfig(lattice_beam=0.41)).lattice.num_arcs == 6
+
+
+def test_error_paths():
+    w1 = lb.load_wfst_text("0 1 1 1 0.5\n0 2 2 2 1.0\n1 0.0\n2 0.0\n")
+    with pytest.raises(lb.DecodeFailure):
+        lb.decode_utterance(w1, lb.load_cost_matrix("2 2\n0.3 0.1\n0.3 0.1\n"))
+    with pytest.raises(lb.UsageError, match="label"):
+        lb.decode_utterance(w1, lb.load_cost_matrix("1 1\n0.3\n"))
+    part = lb.decode_utterance(lb.load_wfst_text("0 1 1 1 0.5\n2 0.0\n"), lb.load_cost_matrix("1 1\n0.3\n"))
+    assert part.partial and part.words == [1] and part.total_cost == pytest.approx(0.8)
+    g = synthetic.uniform_bench_graph(0, num_states=500, arcs_per_state=5, num_labels=40)
+    m = synthetic.bench_matrix(1, num_frames=10, num_labels=40)
+    with pytest.raises(lb.CapacityError) as e:
+        lb.decode_utterance(g, m, lb.DecodeConfig(beam=13.0, max_tokens_per_frame=5))
+    assert e.value.bound == "--max-tokens-per-frame"
+    with pytest.raises(lb.CapacityError) as e:
+        lb.decode_utterance(g, m, lb.DecodeConfig(beam=13.0, max_lattice_arcs=100))
+    assert e.value.bound == "--max-lattice-arcs"
+
+
+def test_expand_single_ops(oracle_mod):
+    for seed in range(40):
+        w, m = synthetic.random_task(seed)
+        s, c, cut = lb.expand_emitting(w, np.array([w.start_state]), np.array([0.0]), m, 0, 6.0)
+        rs, rc, rcut = oracle_mod.expand_emitting(w, [w.start_state], [0.0], m.costs[0], 6.0)
+        assert np.array_equal(s, rs) and np.array_equal(c, rc) and (cut == rcut or
+                                                                     (math.isinf(cut) and math.isinf(rcut)))
+    chain = lb.load_wfst_text("0 1 0 0 0.3\n1 2 0 0 0.4\n2 0.0\n")
+    s, c = lb.expand_nonemitting(chain, np.array([0]), np.array([0.5]), 100.0)
+    assert s.tolist() == [0, 1, 2] and c == pytest.approx([0.5, 0.8, 1.2])
+    s, c = lb.expand_nonemitting(chain, np.array([0]), np.array([0.5]), 1.0)
+    assert s.tolist() == [0, 1]
+    cyc = lb.load_wfst_text("0 1 0 0 0.0\n1 0 0 0 0.0\n0 0.0\n1 0.0\n")
+    s, c = lb.expand_nonemitting(cyc, np.array([0]), np.array([0.2]), 100.0)
+    assert s.tolist() == [0, 1] and c == pytest.approx([0.2, 0.2])
+    for seed in range(40):
+        w, _ = synthetic.random_task(seed)
+        st = np.arange(0, w.num_states, 3)
+        co = np.linspace(0.0, 2.0, len(st))
+        s, c = lb.expand_nonemitting(w, st, co, 4.0)
+        rs, rc = oracle_mod.expand_nonemitting(w, st, co, 4.0)
+        assert np.array_equal(s, rs) and np.array_equal(c, rc)
+
+
+@pytest.mark.parametrize("S,deg,L,beam,ma", [(2000, 5, 100, 10.0, 300), (3000, 4, 60, 12.0, 500)])
+def test_max_active_uniform(oracle_mod, S, deg, L, beam, ma):
+    w = synthetic.uniform_bench_graph(1, num_states=S, arcs_per_state=deg, num_labels=L)
+    for u in range(3):
+        m = synthetic.bench_matrix(300 + u, num_frames=30, num_labels=L)
+        got, ref = decode_both(w, m, oracle_mod, beam, 6.0, max_active=ma)
+        check_pair(got, ref, 6.0)
+
+
+def test_config1_frames(oracle_mod):
+    """Config C1 graph (uniform 10k x 5, 500 labels, beam 13), 2 utterances x 60 frames."""
+    w = synthetic.config_graph("C1")
+    for u in range(2):
+        m = synthetic.bench_matrix(100 + u, num_frames=60, num_labels=500)
+        got, ref = decode_both(w, m, oracle_mod, 13.0, 8.0, want_lattice=(u == 0))
+        check_pair(got, ref, 8.0, want_lattice=(u == 0))
+
+
+def test_hclg_with_epsilon_and_max_active(oracle_mod):
+    w = synthetic.hclg_graph(3, num_states=300_000, pool_size=4000, num_pdfs=500)
+    for u in range(2):
+        m = synthetic.hclg_matrix(40 + u, num_frames=40, num_pdfs=500)
+        got, ref = decode_both(w, m, oracle_mod, 13.0, 8.0, max_active=2000, want_lattice=(u == 0))
+        check_pair(got, ref, 8.0, want_lattice=(u == 0))
+
+
+def test_batch_equals_single(oracle_mod):
+    w = synthetic.uniform_bench_graph(0, num_states=2000, arcs_per_state=5, num_labels=80)
+    mats = [synthetic.bench_matrix(100 + i, num_frames=20 + 3 * i, num_labels=80) for i in range(10)]
+    cfg = lb.DecodeConfig(beam=9.0, lattice_beam=2.0, lanes=3)
+    bat = lb.decode_batch(w, mats, cfg)
+    for m, b in zip(mats, bat):
+        s = lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0, lattice_beam=2.0))
+        assert s.words == b.words and s.total_cost == b.total_cost
+        assert lb.write_lattice_text(s.lattice) == lb.write_lattice_text(b.lattice)
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 9.0)
+    assert all(st == 0) and [r.total_cost for r in bat] == tc.tolist()
+
+
+def test_reference_wfst_object_duck_typing(oracle_mod):
+    """Any object with the reference Wfst attributes decodes (drop-in)."""
+    w, m = synthetic.random_task(5)
+
+    class Duck:
+        pass
+    d = Duck()
+    for k in ("num_states", "start_state", "arc_offsets", "arc_src", "arc_dst", "arc_ilabel",
+              "arc_olabel", "arc_weight", "final_cost_array", "max_ilabel", "num_arcs"):
+        setattr(d, k, getattr(w, k))
+    r1 = lb.decode_utterance(d, m, lb.DecodeConfig(beam=8.0), want_lattice=False)
+    r2 = lb.decode_utterance(w, m, lb.DecodeConfig(beam=8.0), want_lattice=False)
+    assert r1.words == r2.words and r1.total_cost == r2.total_cost
