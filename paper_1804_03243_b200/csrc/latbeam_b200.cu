@@ -60,9 +60,8 @@ struct Workspace {
     int path_cap = 0, tmax = 0;
     bool packs = false, lat = false;
     // lane scratch
-    unsigned long long *pack = nullptr;
-    double *cost = nullptr, *minsnap = nullptr, *fc0 = nullptr, *fc1 = nullptr;
-    int *pred = nullptr, *tokidx = nullptr;
+    StateRec *rec = nullptr;
+    double *minsnap = nullptr, *fc0 = nullptr, *fc1 = nullptr;
     unsigned *tag = nullptr, *touched = nullptr, *fs0 = nullptr, *fs1 = nullptr, *round_ctr = nullptr;
     // slots
     unsigned *tok_state = nullptr;
@@ -91,7 +90,8 @@ struct lb_graph {
     int32_t start = 0, max_ilabel = 0;
     int sms = 148;
     int4 *arcs = nullptr;
-    unsigned *src = nullptr, *ol = nullptr, *off = nullptr, *eoff = nullptr, *eids = nullptr;
+    unsigned *src = nullptr, *ol = nullptr, *off = nullptr, *eoff = nullptr;
+    int4 *eps = nullptr;
     double *fin = nullptr;
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
@@ -108,7 +108,7 @@ struct lb_graph {
         g.ol = ol;
         g.off = off;
         g.eoff = eoff;
-        g.eids = eids;
+        g.eps = eps;
         g.fin = fin;
         g.S = (int)S;
         g.start = start;
@@ -146,13 +146,10 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
         if (e == cudaSuccess) w.owned.push_back((void *)*p);
         return e;
     };
-    CK(A(&w.pack, S * nl));
-    CK(A(&w.cost, S * nl));
-    CK(A(&w.minsnap, S * nl));
+    CK(A(&w.rec, S * nl));
+    if (lat) CK(A(&w.minsnap, S * nl));
     CK(A(&w.fc0, S * nl));
     CK(A(&w.fc1, S * nl));
-    CK(A(&w.pred, S * nl));
-    CK(A(&w.tokidx, S * nl));
     CK(A(&w.tag, S * nl));
     CK(A(&w.touched, S * nl));
     CK(A(&w.fs0, S * nl));
@@ -181,20 +178,18 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
     CK(A(&w.out_c, 8 * nl));
     CK(A(&w.d_lanes, nl));
     CK(A(&w.d_desc, nl));
-    CK(cudaMemsetAsync(w.pack, 0xFF, S * nl * 8, g->stream));
-    CK(cudaMemsetAsync(w.tokidx, 0, S * nl * 4, g->stream));
+    CK(cudaMemsetAsync(w.rec, 0xFF, S * nl * sizeof(StateRec), g->stream));
     CK(cudaMemsetAsync(w.tag, 0, S * nl * 4, g->stream));
     CK(cudaMemsetAsync(w.round_ctr, 0, nl * 4, g->stream));
-    fill_f64<<<g->sms * 4, 256, 0, g->stream>>>(w.minsnap, INFINITY, (long long)(S * nl));
-    CK(cudaGetLastError());
+    if (lat) {
+        fill_f64<<<g->sms * 4, 256, 0, g->stream>>>(w.minsnap, INFINITY, (long long)(S * nl));
+        CK(cudaGetLastError());
+    }
     std::vector<LaneWs> hl(nl);
     for (size_t l = 0; l < nl; l++) {
         LaneWs &x = hl[l];
-        x.pack = w.pack + l * S;
-        x.cost = w.cost + l * S;
-        x.pred = w.pred + l * S;
-        x.tokidx = w.tokidx + l * S;
-        x.minsnap = w.minsnap + l * S;
+        x.rec = w.rec + l * S;
+        x.minsnap = lat ? w.minsnap + l * S : nullptr;
         x.tag = w.tag + l * S;
         x.touched = w.touched + l * S;
         x.fs0 = w.fs0 + l * S;
@@ -338,7 +333,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 1024;
     // lanes: requested, else as many as fit a memory budget (<= 2 waves of SMs)
-    const size_t per_lane = (size_t)S * 64 + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
+    const size_t per_lane = (size_t)S * (64 + (lat ? 8 : 0)) + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
                             (size_t)lat_cap * 28 + (size_t)path_cap * 4 + (size_t)(tmax + 2) * 16 + 256;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -365,7 +360,13 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const size_t acrow_bytes = (size_t)D * 8;
     p.acrow_smem = acrow_bytes <= 160 * 1024;
     const size_t smem = p.acrow_smem ? acrow_bytes : 0;
-    CK(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    // decode-lane variants: CTA size x batch width (all spill-free at their register budget)
+    void (*kern)(GraphDev, Params, const LaneWs *, const UttDesc *, int) = decode_kernel<1024, 2>;
+    if (threads == 768) kern = decode_kernel<768, 2>;
+    else if (threads == 512) kern = decode_kernel<512, 4>;
+    else if (threads == 256) kern = decode_kernel<256, 4>;
+    else if (threads != 1024) return set_err(LB_USAGE, "threads_per_lane must be 256, 512, 768 or 1024");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();
 
     cudaEvent_t e0, e1, e2, e3;
@@ -386,7 +387,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaMemcpyAsync(w.d_desc, desc.data(), nw * sizeof(UttDesc), cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(w.out_i, 0, 8 * sizeof(int) * nw, st));
         CK(cudaEventRecord(e0, st));
-        decode_kernel<<<nw, threads, smem, st>>>(gd, p, w.d_lanes, w.d_desc, nw);
+        kern<<<nw, threads, smem, st>>>(gd, p, w.d_lanes, w.d_desc, nw);
         CK(cudaGetLastError());
         res->launches++;
         CK(cudaEventRecord(e1, st));
@@ -501,18 +502,27 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     // host-side packing of the device layout
     std::vector<int4> arcs((size_t)A);
     std::vector<unsigned> hsrc((size_t)A), hol((size_t)A), hoff((size_t)S + 1), heoff((size_t)S + 1);
-    std::vector<unsigned> heids;
+    std::vector<int4> heps;
     int32_t maxil = 0;
     for (int64_t s = 0; s < S; s++) {
         hoff[s] = (unsigned)off[s];
-        heoff[s] = (unsigned)heids.size();
+        heoff[s] = (unsigned)heps.size();
         if (off[s + 1] < off[s]) return set_err(LB_USAGE, "arc offsets must be non-decreasing");
         for (int64_t a = off[s]; a < off[s + 1]; a++) {
-            if (il[a] == 0) heids.push_back((unsigned)a);
+            if (il[a] == 0) {
+                long long bits;
+                std::memcpy(&bits, &w[a], 8);
+                int4 r;
+                r.x = dst[a];
+                r.y = (int)a;
+                r.z = (int)(bits & 0xFFFFFFFFll);
+                r.w = (int)(bits >> 32);
+                heps.push_back(r);
+            }
         }
     }
     hoff[S] = (unsigned)A;
-    heoff[S] = (unsigned)heids.size();
+    heoff[S] = (unsigned)heps.size();
     for (int64_t a = 0; a < A; a++) {
         if (dst[a] < 0 || dst[a] >= S || il[a] < 0 || ol[a] < 0)
             return set_err(LB_USAGE, "arc field out of range");
@@ -530,22 +540,22 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
         maxil = std::max(maxil, il[a]);
     }
     g->max_ilabel = maxil;
-    g->E = (int64_t)heids.size();
+    g->E = (int64_t)heps.size();
     CK(dalloc(&g->arcs, A));
     CK(dalloc(&g->src, A));
     CK(dalloc(&g->ol, A));
     CK(dalloc(&g->off, S + 1));
     CK(dalloc(&g->eoff, S + 1));
-    CK(dalloc(&g->eids, g->E));
+    CK(dalloc(&g->eps, g->E));
     CK(dalloc(&g->fin, S));
     CK(cudaMemcpy(g->arcs, arcs.data(), sizeof(int4) * A, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->src, hsrc.data(), 4 * A, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->ol, hol.data(), 4 * A, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->off, hoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->eoff, heoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
-    if (g->E) CK(cudaMemcpy(g->eids, heids.data(), 4 * g->E, cudaMemcpyHostToDevice));
+    if (g->E) CK(cudaMemcpy(g->eps, heps.data(), sizeof(int4) * g->E, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->fin, fin, 8 * S, cudaMemcpyHostToDevice));
-    g->bytes = A * 16 + A * 8 + (S + 1) * 8 + g->E * 4 + S * 8;
+    g->bytes = A * 16 + A * 8 + (S + 1) * 8 + g->E * 16 + S * 8;
     *out = g.release();
     return LB_OK;
 }
@@ -559,7 +569,7 @@ int lb_graph_destroy(lb_graph *g) {
     cudaFree(g->ol);
     cudaFree(g->off);
     cudaFree(g->eoff);
-    cudaFree(g->eids);
+    cudaFree(g->eps);
     cudaFree(g->fin);
     cudaFree(g->d_costs);
     if (g->h_stage) cudaFreeHost(g->h_stage);
@@ -751,7 +761,7 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     LaneWs L;
     CK(cudaMemcpyAsync(&L, w.d_lanes, sizeof(LaneWs), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (mode == 0) set_tokidx<<<(int)((n + 255) / 256), 256, 0, st>>>(L.tokidx, d.tok_state, (int)n);
+    if (mode == 0) setup_tokens<<<(int)((n + 255) / 256), 256, 0, st>>>(L.rec, d.tok_state, d.tok_cost, (int)n);
     Params p;
     std::memset(&p, 0, sizeof(p));
     p.beam = beam;

@@ -33,14 +33,16 @@ enum : int {
     E_INT_PRUNE_EPS = 11,    // InternalInvariantError: eps extra-cost fixpoint
 };
 
-// Graph replica in HBM.  Arc record = 16 B {dst, ilabel, weight}.
+// Graph replica in HBM.  Arc record = 16 B {dst, ilabel, weight};
+// epsilon arcs additionally get a per-state CSR of 16 B {dst, arc id, weight}
+// records so the closure reads one record per epsilon arc.
 struct GraphDev {
     const int4 *arcs;
     const unsigned *src;
     const unsigned *ol;
     const unsigned *off;    // [S+1]
-    const unsigned *eoff;   // [S+1] epsilon-arc index
-    const unsigned *eids;   // epsilon arc ids, arc-id order per state
+    const unsigned *eoff;   // [S+1] epsilon CSR offsets
+    const int4 *eps;        // epsilon records {dst, arc, w_lo, w_hi}
     const double *fin;      // final cost, +inf = non-final
     int S;
     int start;
@@ -48,12 +50,19 @@ struct GraphDev {
     int _pad;
 };
 
+// Per-state record of a lane: everything a touched state needs in ONE 32-byte
+// sector.  cost[] is double-buffered by frame parity so the previous frame's
+// token cost of a source state stays readable while the current frame writes.
+struct __align__(32) StateRec {
+    unsigned long long pack;   // packed (cost, arc) word, SENT = untouched
+    double cost[2];            // f64 winner cost of frame t in cost[t & 1]
+    int pred;                  // (prev token index << 1) | 1  or  (source state << 1)
+    int tokidx;                // token index in the newest frame (sparse-set check)
+};
+
 // Per-lane scratch, all indexed by state (O(S) once, reset O(touched) per frame).
 struct LaneWs {
-    unsigned long long *pack;
-    double *cost;
-    int *pred;              // emit: prev-frame token index; eps: source state
-    int *tokidx;            // state -> token index in the newest frame (sparse-set)
+    StateRec *rec;
     double *minsnap;        // min frontier snapshot cost this frame (lattice eps rule)
     unsigned *tag;          // epsilon round tag
     unsigned *touched;
@@ -110,6 +119,25 @@ __device__ __forceinline__ double dec64(unsigned long long e) {
     unsigned long long u = (e >> 63) ? (e ^ 0x8000000000000000ull) : ~e;
     return __longlong_as_double((long long)u);
 }
+struct RecView {
+    unsigned long long pack;
+    double cost0, cost1;
+    int pred, tokidx;
+    __device__ __forceinline__ double cost(int parity) const { return parity ? cost1 : cost0; }
+};
+
+__device__ __forceinline__ RecView load_rec(const StateRec *r) {
+    const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2 *>(r));
+    const ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2 *>(r) + 1);
+    RecView v;
+    v.pack = a.x;
+    v.cost0 = __longlong_as_double((long long)a.y);
+    v.cost1 = __longlong_as_double((long long)b.x);
+    v.pred = (int)(unsigned)(b.y & 0xFFFFFFFFull);
+    v.tokidx = (int)(unsigned)(b.y >> 32);
+    return v;
+}
+
 __device__ __forceinline__ void load_arc(const int4 *arcs, unsigned a, unsigned &dst, unsigned &il,
                                          double &w) {
     int4 r = __ldg(arcs + a);

@@ -4,43 +4,52 @@
 // sequence parallelism, as lanes instead of MPS processes).
 // A lane walks the utterance's frames in order; inside a frame the CTA runs the
 // phases below, separated by __syncthreads (no grid-wide sync, no host round
-// trip per frame):
+// trip per frame).  Every per-state access of a phase lands in the state's one
+// 32-byte StateRec sector, and the hot loops are batched 4-wide so each thread
+// keeps 4 independent gathers / atomics in flight.
 //
 //   emit      warp-cooperative expansion of the previous frame's tokens: the warp
 //             takes 32 tokens, prefix-scans their out-degrees with shuffles
 //             (Alg. 2 / static partition, scheduler.py:60-78) and walks the
-//             flattened arc range 32 arcs at a time, each lane binary-searching
-//             its owner token with shuffles; 16 B arc loads; one 64-bit atomicMin
-//             per candidate on the packed (cost, arc) word (Alg. 1,
-//             decoder.py:189-205); states seen for the first time (old ==
-//             sentinel) are appended to the touched list with one shared atomic
+//             flattened arc range 128 arcs at a time (4 per lane), each lane
+//             binary-searching its owner token with shuffles; 16 B arc loads;
+//             one 64-bit atomicMin per candidate on the packed (cost, arc) word
+//             (Alg. 1, decoder.py:189-205); states seen for the first time
+//             (old == sentinel) go to the touched list with one shared atomic
 //             per warp.  The frame best is a block min over ALL candidates.
 //   winners   per touched state: the winner's f64 cost is recomputed from its
-//             arc (same operands, same order => bit-identical to the offer) and
-//             the state is seeded if cost <= cutoff; max-active histogram.
+//             arc and its source token's cost (the same operands in the same
+//             order => bit-identical to the offer) and the state is seeded if
+//             cost <= cutoff; max-active histogram.
 //   epsilon   Jacobi rounds (reference.py:160-192): phase A offers pack words
-//             from snapshot costs, phase B lets the unique winning offer of the
-//             round write the state's f64 cost / source.
+//             from snapshot costs, phase B lets the round's unique winning offer
+//             write the state's f64 cost / source.
 //   aggregate touched states under the cutoff become the frame's token list
-//             (device order; the host sorts by state when lists are read back).
+//             (device order; the host sorts by state when lists are read back);
+//             the same pass resets the state's pack word (O(touched), not O(S)).
 //   lattice   live arcs by rule A.5: emitting arc live iff its
 //             candidate <= cutoff and its destination was kept; epsilon arc live
 //             iff both ends kept and min-snapshot(src) + w <= cutoff.
-//   reset     O(touched) reset of the per-state words (not O(S), decoder.py:123).
 #pragma once
 #include "lb_device.cuh"
 
 namespace lbk {
 
+
 struct Smem {
-    int ntouched, nfront, nnext, ntok, nlat, err, err_frame, moved;
+    int ntouched, nfront, nnext, ntok, nlat, nfix, err, err_frame;
     long long err_aux;
     double cutoff;
+    unsigned round_id;      // epsilon round tag (persistent per lane)
+    int fpar;               // which frontier buffer is current
+    unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
     double red[32];
     long long lred[32];
     int ired[32];
     int hist[NBINS];
 };
+
+__device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7FF0000000000000ll); }
 
 __device__ __forceinline__ double block_min(double v, Smem &sm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -48,7 +57,7 @@ __device__ __forceinline__ double block_min(double v, Smem &sm) {
     if (lane == 0) sm.red[warp] = v;
     __syncthreads();
     if (warp == 0) {
-        double x = lane < nw ? sm.red[lane] : __longlong_as_double(0x7FF0000000000000ll);
+        double x = lane < nw ? sm.red[lane] : inf_d();
         x = warp_min(x);
         if (lane == 0) sm.red[0] = x;
     }
@@ -83,7 +92,7 @@ __device__ __forceinline__ void block_argmin(double &v, int &s, Smem &sm) {
     if (lane == 0) { sm.red[warp] = v; sm.ired[warp] = s; }
     __syncthreads();
     if (warp == 0) {
-        double x = lane < nw ? sm.red[lane] : __longlong_as_double(0x7FF0000000000000ll);
+        double x = lane < nw ? sm.red[lane] : inf_d();
         int y = lane < nw ? sm.ired[lane] : 0x7FFFFFFF;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -100,10 +109,12 @@ __device__ __forceinline__ void block_argmin(double &v, int &s, Smem &sm) {
 }
 
 // Warp-cooperative load-balanced walk over every (token, out-arc) pair of a
-// token list.  f(i, arc, token_cost) runs once per pair (possibly divergent).
-template <class F>
-__device__ __forceinline__ void for_each_token_arc(const GraphDev &g, const unsigned *ts,
-                                                   const double *tc, int n, unsigned &c_scan, F &&f) {
+// token list, UNR arcs per lane per batch.  f(valid[], i[], arc[], cost[])
+// receives one batch (the per-slot arrays are fully unrolled registers).
+template <int UNR, class F>
+__device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, const unsigned *ts,
+                                                           const double *tc, int n, unsigned &c_scan,
+                                                           F &&f) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int base = warp * 32; base < n; base += nw * 32) {
         const int i = base + lane;
@@ -122,23 +133,34 @@ __device__ __forceinline__ void for_each_token_arc(const GraphDev &g, const unsi
         const int excl = incl - deg;
         const int total = __shfl_sync(FULL, incl, 31);
         if (lane == 0) c_scan += (unsigned)total;
-        for (int j0 = 0; j0 < total; j0 += 32) {
-            const int j = j0 + lane;
-            int k = 0;
+        for (int j0 = 0; j0 < total; j0 += 32 * UNR) {
+            bool vv[UNR];
+            int ii[UNR];
+            unsigned aa[UNR];
+            double cc[UNR];
 #pragma unroll
-            for (int b = 16; b > 0; b >>= 1) {
-                int t = __shfl_sync(FULL, incl, k + b - 1);
-                if (t <= j) k += b;
+            for (int u = 0; u < UNR; u++) {
+                const int j = j0 + u * 32 + lane;
+                int k = 0;
+#pragma unroll
+                for (int b = 16; b > 0; b >>= 1) {
+                    int t = __shfl_sync(FULL, incl, k + b - 1);
+                    if (t <= j) k += b;
+                }
+                const int ek = __shfl_sync(FULL, excl, k);
+                const unsigned lk = __shfl_sync(FULL, lo, k);
+                cc[u] = __shfl_sync(FULL, c, k);
+                vv[u] = j < total;
+                ii[u] = base + k;
+                aa[u] = lk + (unsigned)(j - ek);
             }
-            const int ek = __shfl_sync(FULL, excl, k);
-            const unsigned lk = __shfl_sync(FULL, lo, k);
-            const double ck = __shfl_sync(FULL, c, k);
-            if (j < total) f(base + k, lk + (unsigned)(j - ek), ck);
+            f(vv, ii, aa, cc);
         }
     }
 }
 
-// Per-CTA decode state.  All members are block-uniform except the counters.
+// Per-CTA decode state (block-uniform).  UNR = independent items per thread per batch.
+template <int UNR>
 struct Lane {
     const GraphDev &g;
     const Params &p;
@@ -147,16 +169,17 @@ struct Lane {
     Smem &sm;
     double *acrow;          // shared-memory row (when p.acrow_smem)
     const double *row;      // global row of the current frame
-    unsigned *fs, *fsn;
-    double *fc, *fcn;
-    unsigned round_id;
-    unsigned c_scan = 0, c_cand = 0, c_escan = 0, c_ecand = 0;
-    long long c_tok = 0, c_front = 0, c_next = 0;
+    int par;                // parity of the current frame (cost slot)
 
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
                     Smem &sm_, double *acrow_)
-        : g(g_), p(p_), L(L_), io(io_), sm(sm_), acrow(acrow_), row(nullptr), fs(L_.fs0),
-          fsn(L_.fs1), fc(L_.fc0), fcn(L_.fc1), round_id(0) {}
+        : g(g_), p(p_), L(L_), io(io_), sm(sm_), acrow(acrow_), row(nullptr), par(0) {}
+
+    // current / next frontier buffers (block-uniform selector in shared memory)
+    __device__ __forceinline__ unsigned *fs() const { return sm.fpar ? L.fs1 : L.fs0; }
+    __device__ __forceinline__ unsigned *fsn() const { return sm.fpar ? L.fs0 : L.fs1; }
+    __device__ __forceinline__ double *fc() const { return sm.fpar ? L.fc1 : L.fc0; }
+    __device__ __forceinline__ double *fcn() const { return sm.fpar ? L.fc0 : L.fc1; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
         return p.acrow_smem ? acrow[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
@@ -177,49 +200,101 @@ struct Lane {
 
     // ---- emit: returns the block-wide best candidate ----
     __device__ double emit(const unsigned *pts, const double *ptc, int np) {
-        double lbest = __longlong_as_double(0x7FF0000000000000ll);
-        for_each_token_arc(g, pts, ptc, np, c_scan, [&](int, unsigned a, double ck) {
-            unsigned dst, il;
-            double w;
-            load_arc(g.arcs, a, dst, il, w);
-            if (il == 0) return;
-            c_cand++;
-            const double cand = __dadd_rn(__dadd_rn(ck, w), ac(il));
-            lbest = fmin(lbest, cand);
-            const unsigned long long word = pack_word(cand, a);
-            const unsigned long long old = atomicMin(L.pack + dst, word);
-            if (old == SENT) {
-                const int sl = agg_append(&sm.ntouched);
-                __stcg(L.touched + sl, dst);
+        double lbest = inf_d();
+        StateRec *rec = L.rec;
+        unsigned c_scan = 0, c_cand = 0;
+        for_each_token_arc_batched<UNR>(g, pts, ptc, np, c_scan,
+                                   [&](const bool *vv, const int *, const unsigned *aa, const double *cc) {
+            int4 r[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++)
+                if (vv[u]) r[u] = __ldg(g.arcs + aa[u]);
+            unsigned long long old[UNR];
+            bool em[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                em[u] = vv[u] && r[u].y != 0;
+                if (em[u]) {
+                    const double w = __hiloint2double(r[u].w, r[u].z);
+                    const double cand = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r[u].y));
+                    lbest = fmin(lbest, cand);
+                    old[u] = atomicMin(&rec[r[u].x].pack, pack_word(cand, aa[u]));
+                    c_cand++;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (em[u] && old[u] == SENT) {
+                    const int sl = agg_append(&sm.ntouched);
+                    __stcg(L.touched + sl, (unsigned)r[u].x);
+                }
             }
         });
+        c_cand = warp_sum(c_cand);
+        c_scan = warp_sum(c_scan);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&sm.c_cand, (unsigned long long)c_cand);
+            atomicAdd(&sm.c_scan, (unsigned long long)c_scan);
+        }
         return block_min(lbest, sm);
     }
 
     // ---- winners: f64 cost of every touched state; seed frontier; histogram ----
-    __device__ void winners(const double *ptc, double cutoff, double best) {
+    __device__ void winners(double cutoff, double best) {
         const int nt = sm.ntouched;
         const bool hist = p.max_active > 0;
         const double width = __ddiv_rn(p.beam, (double)NBINS);
-        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
-            const unsigned v = __ldcg(L.touched + k);
-            const unsigned a = (unsigned)__ldcg(L.pack + v);
-            unsigned dst, il;
-            double w;
-            load_arc(g.arcs, a, dst, il, w);
-            const unsigned src = __ldg(g.src + a);
-            const int i = __ldcg(L.tokidx + src);
-            const double cand = __dadd_rn(__dadd_rn(__ldcg(ptc + i), w), ac(il));
-            __stcg(L.cost + v, cand);
-            __stcg(L.pred + v, i);
-            if (cand <= cutoff) {
-                const int sl = agg_append(&sm.nfront);
-                __stcg(fs + sl, v);
-                __stcg(fc + sl, cand);
-                if (hist) {
-                    const double q = __ddiv_rn(__dsub_rn(cand, best), width);
-                    const int bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
-                    atomicAdd(&sm.hist[bin], 1);
+        const int pp = par ^ 1;
+        StateRec *rec = L.rec;
+        unsigned *fs = this->fs();
+        double *fc = this->fc();
+        for (int k0 = threadIdx.x; k0 < nt; k0 += UNR * blockDim.x) {
+            unsigned v[UNR];
+            bool ok[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                const int k = k0 + u * blockDim.x;
+                ok[u] = k < nt;
+                v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
+            }
+            unsigned a[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) a[u] = ok[u] ? (unsigned)__ldcg(&rec[v[u]].pack) : 0u;
+            unsigned il[UNR], src[UNR];
+            double w[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (ok[u]) {
+                    const int2 lo = __ldg(reinterpret_cast<const int2 *>(g.arcs + a[u]) + 0);
+                    il[u] = (unsigned)lo.y;
+                    w[u] = __ldg(reinterpret_cast<const double *>(g.arcs + a[u]) + 1);
+                    src[u] = __ldg(g.src + a[u]);
+                }
+            }
+            double pc[UNR];
+            int pi[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (ok[u]) {
+                    pc[u] = __ldcg(&rec[src[u]].cost[pp]);
+                    pi[u] = __ldcg(&rec[src[u]].tokidx);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (!ok[u]) continue;
+                const double cand = __dadd_rn(__dadd_rn(pc[u], w[u]), ac(il[u]));
+                __stcg(&rec[v[u]].cost[par], cand);
+                __stcg(&rec[v[u]].pred, (pi[u] << 1) | 1);
+                if (cand <= cutoff) {
+                    const int sl = agg_append(&sm.nfront);
+                    __stcg(fs + sl, v[u]);
+                    __stcg(fc + sl, cand);
+                    if (hist) {
+                        const double q = __ddiv_rn(__dsub_rn(cand, best), width);
+                        const int bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
+                        atomicAdd(&sm.hist[bin], 1);
+                    }
                 }
             }
         }
@@ -268,34 +343,49 @@ struct Lane {
         return r;
     }
 
+    // called by one thread between barriers
+    __device__ __forceinline__ void swap_frontier() { sm.fpar ^= 1; }
+
     // Keep frontier entries with cost <= cutoff (after a max-active tightening).
     __device__ void filter_frontier(double cutoff) {
         const int nf = sm.nfront;
-        for (int k = threadIdx.x; k < nf; k += blockDim.x) {
-            const double c = __ldcg(fc + k);
-            if (c <= cutoff) {
-                const int sl = agg_append(&sm.nnext);
-                __stcg(fsn + sl, __ldcg(fs + k));
-                __stcg(fcn + sl, c);
+        unsigned *fs = this->fs(), *fsn = this->fsn();
+        double *fc = this->fc(), *fcn = this->fcn();
+        for (int k0 = threadIdx.x; k0 < nf; k0 += UNR * blockDim.x) {
+            double c[UNR];
+            unsigned s[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                const int k = k0 + u * blockDim.x;
+                if (k < nf) {
+                    c[u] = __ldcg(fc + k);
+                    s[u] = __ldcg(fs + k);
+                } else {
+                    c[u] = inf_d();
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (c[u] <= cutoff) {
+                    const int sl = agg_append(&sm.nnext);
+                    __stcg(fsn + sl, s[u]);
+                    __stcg(fcn + sl, c[u]);
+                }
             }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             sm.nfront = sm.nnext;
             sm.nnext = 0;
+            swap_frontier();
         }
-        swap_frontier();
         __syncthreads();
-    }
-
-    __device__ __forceinline__ void swap_frontier() {
-        unsigned *t = fs; fs = fsn; fsn = t;
-        double *u = fc; fc = fcn; fcn = u;
     }
 
     // ---- epsilon closure under a fixed cutoff (Jacobi rounds) ----
     __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
+        StateRec *rec = L.rec;
         long long rounds = 0;
         for (;;) {
             const int nf = sm.nfront;
@@ -305,8 +395,10 @@ struct Lane {
                 __syncthreads();
                 return false;
             }
-            ++round_id;
-            c_front += nf;
+            const unsigned round_id = sm.round_id + 1;
+            unsigned *fs = this->fs(), *fsn = this->fsn();
+            double *fc = this->fc(), *fcn = this->fcn();
+            unsigned c_escan = 0, c_ecand = 0;
             // phase A: offers from snapshot costs
             for (int k = threadIdx.x; k < nf; k += blockDim.x) {
                 const unsigned u = __ldcg(fs + k);
@@ -318,15 +410,13 @@ struct Lane {
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
                 c_escan += e1 - e0;
                 for (unsigned e = e0; e < e1; ++e) {
-                    const unsigned a = __ldg(g.eids + e);
-                    unsigned v, il;
-                    double w;
-                    load_arc(g.arcs, a, v, il, w);
-                    const double cand = __dadd_rn(cu, w);
+                    const int4 r = __ldg(g.eps + e);
+                    const double cand = __dadd_rn(cu, __hiloint2double(r.w, r.z));
                     if (!(cand <= cutoff)) continue;
                     c_ecand++;
-                    const unsigned long long word = pack_word(cand, a);
-                    const unsigned long long old = atomicMin(L.pack + v, word);
+                    const unsigned v = (unsigned)r.x;
+                    const unsigned long long word = pack_word(cand, (unsigned)r.y);
+                    const unsigned long long old = atomicMin(&rec[v].pack, word);
                     if (old == SENT) {
                         const int sl = agg_append(&sm.ntouched);
                         __stcg(L.touched + sl, v);
@@ -337,6 +427,12 @@ struct Lane {
                     }
                 }
             }
+            c_escan = warp_sum(c_escan);
+            c_ecand = warp_sum(c_ecand);
+            if ((threadIdx.x & 31) == 0) {
+                atomicAdd(&sm.c_escan, (unsigned long long)c_escan);
+                atomicAdd(&sm.c_ecand, (unsigned long long)c_ecand);
+            }
             __syncthreads();
             // phase B: the round's unique winning offer writes cost / source
             for (int k = threadIdx.x; k < nf; k += blockDim.x) {
@@ -344,47 +440,81 @@ struct Lane {
                 const double cu = __ldcg(fc + k);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
                 for (unsigned e = e0; e < e1; ++e) {
-                    const unsigned a = __ldg(g.eids + e);
-                    unsigned v, il;
-                    double w;
-                    load_arc(g.arcs, a, v, il, w);
-                    const double cand = __dadd_rn(cu, w);
+                    const int4 r = __ldg(g.eps + e);
+                    const double cand = __dadd_rn(cu, __hiloint2double(r.w, r.z));
                     if (!(cand <= cutoff)) continue;
-                    if (__ldcg(L.pack + v) == pack_word(cand, a) && __ldcg(L.tag + v) == round_id) {
-                        __stcg(L.cost + v, cand);
-                        __stcg(L.pred + v, (int)u);
+                    const unsigned v = (unsigned)r.x;
+                    if (__ldcg(&rec[v].pack) == pack_word(cand, (unsigned)r.y) &&
+                        __ldcg(L.tag + v) == round_id) {
+                        __stcg(&rec[v].cost[par], cand);
+                        __stcg(&rec[v].pred, (int)(u << 1));
                     }
                 }
             }
             __syncthreads();
             const int nn = sm.nnext;
             for (int k = threadIdx.x; k < nn; k += blockDim.x)
-                __stcg(fcn + k, __ldcg(L.cost + __ldcg(fsn + k)));
+                __stcg(fcn + k, __ldcg(&rec[__ldcg(fsn + k)].cost[par]));
             __syncthreads();
             if (threadIdx.x == 0) {
+                sm.c_front += nf;
+                sm.round_id = round_id;
                 sm.nfront = nn;
                 sm.nnext = 0;
+                swap_frontier();
             }
-            swap_frontier();
             __syncthreads();
         }
     }
 
-    // ---- aggregate: frame token list at io.tok_*[tb ...]; returns token count or -1 ----
+    // ---- aggregate + reset: frame token list at io.tok_*[tb ...]; returns count or -1 ----
     __device__ int aggregate(double cutoff, int frame, long long tb) {
         const int nt = sm.ntouched;
         const long long room = io.tok_cap - tb;
-        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
-            const unsigned v = __ldcg(L.touched + k);
-            const bool init = frame == 0 && (int)v == g.start;
-            const double c = init ? 0.0 : __ldcg(L.cost + v);
-            if (init || c <= cutoff) {
-                const int idx = agg_append(&sm.ntok);
-                if (idx < room) {
-                    __stcg(io.tok_state + tb + idx, v);
-                    __stcg(io.tok_cost + tb + idx, c);
-                    __stcg(L.tokidx + v, idx);
+        StateRec *rec = L.rec;
+        unsigned *fix = fsn();  // scratch: tokens whose predecessor is an epsilon source state
+        for (int k0 = threadIdx.x; k0 < nt; k0 += UNR * blockDim.x) {
+            unsigned v[UNR];
+            bool ok[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                const int k = k0 + u * blockDim.x;
+                ok[u] = k < nt;
+                v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
+            }
+            unsigned long long pk[UNR];
+            double cs[UNR];
+            int pr[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (ok[u]) {
+                    pk[u] = __ldcg(&rec[v[u]].pack);
+                    cs[u] = __ldcg(&rec[v[u]].cost[par]);
+                    pr[u] = __ldcg(&rec[v[u]].pred);
                 }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (!ok[u]) continue;
+                const bool init = frame == 0 && (int)v[u] == g.start;
+                const double c = init ? 0.0 : cs[u];
+                if (init || c <= cutoff) {
+                    const int idx = agg_append(&sm.ntok);
+                    if (idx < room) {
+                        const long long o = tb + idx;
+                        __stcg(io.tok_state + o, v[u]);
+                        __stcg(io.tok_cost + o, c);
+                        __stcg(io.tok_arc + o, init ? -1 : (int)(unsigned)pk[u]);
+                        __stcg(io.tok_pred + o, init ? -1 : pr[u]);
+                        if (p.collect_packs) __stcg(io.tok_pack + o, pk[u]);
+                        __stcg(&rec[v[u]].tokidx, idx);
+                        if (!init && (pr[u] & 1) == 0) {
+                            const int f = agg_append(&sm.nfix);
+                            __stcg(fix + f, (unsigned)idx);
+                        }
+                    }
+                }
+                __stcg(&rec[v[u]].pack, SENT);
             }
         }
         __syncthreads();
@@ -398,26 +528,15 @@ struct Lane {
         }
         __syncthreads();
         if (sm.err) return -1;
-        for (int j = threadIdx.x; j < n; j += blockDim.x) {
-            const unsigned v = __ldcg(io.tok_state + tb + j);
-            const unsigned long long pw = __ldcg(L.pack + v);
-            int arc = -1, pred = -1;
-            if (!(frame == 0 && (int)v == g.start)) {
-                arc = (int)(unsigned)pw;
-                const unsigned il = (unsigned)__ldg(g.arcs + arc).y;
-                const int pr = __ldcg(L.pred + v);
-                if (il > 0) {
-                    pred = (pr << 1) | 1;
-                } else {
-                    const int pi = __ldcg(L.tokidx + pr);
-                    if (pi < 0 || pi >= n || __ldcg(io.tok_state + tb + pi) != (unsigned)pr)
-                        set_error(E_INT_EPS_PRED, frame, v);
-                    pred = pi << 1;
-                }
-            }
-            __stcg(io.tok_arc + tb + j, arc);
-            __stcg(io.tok_pred + tb + j, pred);
-            if (p.collect_packs) __stcg(io.tok_pack + tb + j, pw);
+        // epsilon predecessors: source state -> token index of this frame
+        const int nfx = sm.nfix;
+        for (int q = threadIdx.x; q < nfx; q += blockDim.x) {
+            const long long o = tb + (long long)__ldcg(fix + q);
+            const int u = __ldcg(io.tok_pred + o) >> 1;
+            const int pi = __ldcg(&rec[u].tokidx);
+            if (pi < 0 || pi >= n || __ldcg(io.tok_state + tb + pi) != (unsigned)u)
+                set_error(E_INT_EPS_PRED, frame, u);
+            __stcg(io.tok_pred + o, pi << 1);
         }
         __syncthreads();
         return sm.err ? -1 : n;
@@ -434,39 +553,41 @@ struct Lane {
     }
 
     __device__ __forceinline__ bool kept(unsigned v, long long tb, int n, int &j) const {
-        j = __ldcg(L.tokidx + v);
+        j = __ldcg(&L.rec[v].tokidx);
         return j >= 0 && j < n && __ldcg(io.tok_state + tb + j) == v;
     }
 
-    // ---- lattice arcs of block `frame` (rule A.5) ----
+    // ---- lattice arcs of block `frame` (rule A.5); resets minsnap ----
     __device__ bool lattice(double cutoff, int frame, long long tbp, int np, long long tb, int n,
                             long long lb) {
         if (frame > 0) {
             unsigned dummy = 0;
-            for_each_token_arc(g, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
-                               [&](int i, unsigned a, double ck) {
-                                   unsigned dst, il;
-                                   double w;
-                                   load_arc(g.arcs, a, dst, il, w);
-                                   if (il == 0) return;
-                                   const double cand = __dadd_rn(__dadd_rn(ck, w), ac(il));
-                                   int j;
-                                   if (cand <= cutoff && kept(dst, tb, n, j)) lat_push((int)a, i, j, lb);
-                               });
+            for_each_token_arc_batched<UNR>(g, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
+                                       [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    if (!vv[u]) continue;
+                    const int4 r = __ldg(g.arcs + aa[u]);
+                    if (r.y == 0) continue;
+                    const double w = __hiloint2double(r.w, r.z);
+                    const double cand = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r.y));
+                    int j;
+                    if (cand <= cutoff && kept((unsigned)r.x, tb, n, j)) lat_push((int)aa[u], ii[u], j, lb);
+                }
+            });
         }
         if (g.has_eps) {
+            const double inf = inf_d();
             for (int j = threadIdx.x; j < n; j += blockDim.x) {
                 const unsigned u = __ldcg(io.tok_state + tb + j);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                if (e0 == e1) continue;
                 const double ms = __ldcg(L.minsnap + u);
+                __stcg(L.minsnap + u, inf);
                 for (unsigned e = e0; e < e1; ++e) {
-                    const unsigned a = __ldg(g.eids + e);
-                    unsigned v, il;
-                    double w;
-                    load_arc(g.arcs, a, v, il, w);
+                    const int4 r = __ldg(g.eps + e);
                     int jv;
-                    if (__dadd_rn(ms, w) <= cutoff && kept(v, tb, n, jv)) lat_push((int)a, j, jv, lb);
+                    if (__dadd_rn(ms, __hiloint2double(r.w, r.z)) <= cutoff && kept((unsigned)r.x, tb, n, jv))
+                        lat_push(r.y, j, jv, lb);
                 }
             }
         }
@@ -479,63 +600,68 @@ struct Lane {
         return sm.err == 0;
     }
 
-    // ---- O(touched) reset ----
-    __device__ void reset() {
-        const int nt = sm.ntouched;
-        const bool LAT = p.want_lattice;
-        const double inf = __longlong_as_double(0x7FF0000000000000ll);
-        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
-            const unsigned v = __ldcg(L.touched + k);
-            __stcg(L.pack + v, SENT);
-            if (LAT) __stcg(L.minsnap + v, inf);
-        }
+    // ---- per-frame counter reset (state words were reset in aggregate) ----
+    __device__ void next_frame() {
         for (int b = threadIdx.x; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
         __syncthreads();
         if (threadIdx.x == 0) {
-            sm.ntouched = 0;
-            sm.nfront = 0;
-            sm.nnext = 0;
-            sm.ntok = 0;
-            sm.nlat = 0;
+            sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = 0;
         }
         __syncthreads();
+    }
+
+    // ---- error path: O(touched) reset of every state word this frame touched ----
+    __device__ void reset_touched() {
+        __syncthreads();
+        const int nt = sm.ntouched;
+        const double inf = inf_d();
+        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+            const unsigned v = __ldcg(L.touched + k);
+            __stcg(&L.rec[v].pack, SENT);
+            if (p.want_lattice) __stcg(L.minsnap + v, inf);
+        }
+        next_frame();
     }
 };
 
 // ===========================================================================
 // Full-utterance decode: one CTA per utterance of the wave.
 // ===========================================================================
-__global__ void __launch_bounds__(1024, 1)
+template <int NT, int UNR>
+__global__ void __launch_bounds__(NT, 1)
 decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts,
               int n_utts) {
     __shared__ Smem sm;
     extern __shared__ double s_acrow[];
     if ((int)blockIdx.x >= n_utts) return;
-    const LaneWs L = lanes[blockIdx.x];
-    const UttDesc io = utts[blockIdx.x];
+    const LaneWs &L = lanes[blockIdx.x];
+    const UttDesc &io = utts[blockIdx.x];
     const int tid = threadIdx.x;
     if (tid == 0) {
-        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.err = sm.err_frame = 0;
+        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = sm.err = sm.err_frame = 0;
         sm.err_aux = 0;
+        sm.fpar = 0;
+        sm.round_id = __ldcg(L.round_ctr);
+        sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
     for (int b = tid; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
     __syncthreads();
 
-    Lane ln(g, p, L, io, sm, s_acrow);
-    ln.round_id = __ldcg(L.round_ctr);
+    Lane<UNR> ln(g, p, L, io, sm, s_acrow);
     const int T = io.T;
-    const double inf = __longlong_as_double(0x7FF0000000000000ll);
+    const double inf = inf_d();
     long long tb = 0, lb = 0;
     int ntok = 0, tdone = 0;
 
     // ---- frame 0 (decoder.py:510-523): start token, epsilon closure ----
+    ln.par = 0;
     if (tid == 0) {
-        __stcg(L.pack + g.start, pack_word(0.0, 0u));
-        __stcg(L.cost + g.start, 0.0);
-        __stcg(L.pred + g.start, -1);
+        __stcg(&L.rec[g.start].pack, pack_word(0.0, 0u));
+        __stcg(&L.rec[g.start].cost[0], 0.0);
+        __stcg(&L.rec[g.start].pred, -1);
         __stcg(L.touched, (unsigned)g.start);
-        __stcg(ln.fs, (unsigned)g.start);
-        __stcg(ln.fc, 0.0);
+        __stcg(ln.fs(), (unsigned)g.start);
+        __stcg(ln.fc(), 0.0);
         sm.ntouched = 1;
         sm.nfront = 1;
         io.tok_base[0] = 0;
@@ -544,8 +670,10 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
     __syncthreads();
     double cutoff = __dadd_rn(0.0, p.beam);
     bool ok = ln.epsilon(cutoff, 0);
+    bool reset_done = false;
     if (ok) {
         ntok = ln.aggregate(cutoff, 0, tb);
+        reset_done = true;
         ok = ntok > 0;
     }
     if (ok && p.want_lattice) {
@@ -556,13 +684,15 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         io.tok_base[1] = tb + (ok ? ntok : 0);
         if (p.want_lattice) io.lat_base[1] = lb;
     }
-    ln.reset();
+    if (reset_done) ln.next_frame(); else ln.reset_touched();
 
     for (int t = 1; ok && t <= T; t++) {
         const long long tbp = tb;
         const int np = ntok;
         tb += ntok;
-        ln.c_tok += np;
+        if (tid == 0) sm.c_tok += np;
+        ln.par = t & 1;
+        reset_done = false;
         ln.load_row(io.costs + (long long)(t - 1) * p.D);
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np);
@@ -572,7 +702,7 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
             break;
         }
         cutoff = __dadd_rn(best, p.beam);
-        ln.winners(io.tok_cost + tbp, cutoff, best);
+        ln.winners(cutoff, best);
         __syncthreads();
         if (sm.nfront == 0) {
             if (tid == 0) ln.set_error(E_DEAD_NO_TOKENS, t, 0);
@@ -589,13 +719,11 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         if (g.has_eps) {
             ok = ln.epsilon(cutoff, t);
             if (!ok) break;
-        } else {
-            __syncthreads();
-            if (tid == 0) sm.nfront = 0;
         }
         ntok = ln.aggregate(cutoff, t, tb);
+        reset_done = true;
         if (ntok < 0) { ok = false; break; }
-        ln.c_next += ntok;
+        if (tid == 0) sm.c_next += ntok;
         if (p.want_lattice) {
             ok = ln.lattice(cutoff, t, tbp, np, tb, ntok, lb);
             lb += sm.nlat;
@@ -604,27 +732,25 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
             io.tok_base[t + 1] = tb + ntok;
             if (p.want_lattice) io.lat_base[t + 1] = lb;
         }
-        ln.reset();
+        ln.next_frame();
         tdone = t;
     }
-    if (!ok) ln.reset();
+    if (!ok) {
+        if (reset_done) ln.next_frame(); else ln.reset_touched();
+    }
     __syncthreads();
 
     // ---- counters ----
-    const unsigned long long s_scan = block_sum<unsigned long long>(ln.c_scan, sm);
-    const unsigned long long s_cand = block_sum<unsigned long long>(ln.c_cand, sm);
-    const unsigned long long s_escan = block_sum<unsigned long long>(ln.c_escan, sm);
-    const unsigned long long s_ecand = block_sum<unsigned long long>(ln.c_ecand, sm);
     if (tid == 0) {
-        io.out_c[0] = ln.c_tok;
-        io.out_c[1] = (long long)s_scan;
-        io.out_c[2] = (long long)s_cand;
-        io.out_c[3] = ln.c_front;
-        io.out_c[4] = (long long)s_escan;
-        io.out_c[5] = (long long)s_ecand;
-        io.out_c[6] = ln.c_next;
+        io.out_c[0] = (long long)sm.c_tok;
+        io.out_c[1] = (long long)sm.c_scan;
+        io.out_c[2] = (long long)sm.c_cand;
+        io.out_c[3] = (long long)sm.c_front;
+        io.out_c[4] = (long long)sm.c_escan;
+        io.out_c[5] = (long long)sm.c_ecand;
+        io.out_c[6] = (long long)sm.c_next;
         io.out_c[7] = lb;
-        __stcg(L.round_ctr, ln.round_id);
+        __stcg(L.round_ctr, sm.round_id);
         io.out_i[5] = tdone;
     }
     if (!ok || sm.err) {
@@ -652,7 +778,7 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
     const int bstate = partial ? sc : st;
     if (tid == 0) {
         const double total = partial ? bc : bt;
-        const int bidx = __ldcg(L.tokidx + bstate);
+        const int bidx = __ldcg(&L.rec[bstate].tokidx);
         io.out_i[2] = partial;
         io.out_i[3] = bidx;
         io.out_d[0] = total;
@@ -702,7 +828,7 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
     const int T = io.T;
     const bool partial = io.out_i[2] != 0;
     const double best_total = io.out_d[1];
-    const double inf = __longlong_as_double(0x7FF0000000000000ll);
+    const double inf = inf_d();
     const int D = p.D;
     for (int f = T; f >= 0; f--) {
         const long long b0 = io.tok_base[f];
@@ -799,9 +925,9 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
 
 // ===========================================================================
 // Single-op surfaces (decoder.py:373-435), one CTA.
-//   mode 0 = expand_emitting: tokens at io.tok_*[0..n) with tokidx set; acrow
-//            (scaled) at io.costs; writes (state, cost) winners <= cutoff to
-//            io.tok_state/tok_cost[n ...] and cutoff to io.out_d[0].
+//   mode 0 = expand_emitting: tokens at io.tok_*[0..n), whose states carry
+//            (cost[0], tokidx) from setup_tokens; acrow (scaled) at io.costs;
+//            writes winners <= cutoff to io.tok_state/tok_cost[n ...].
 //   mode 1 = expand_nonemitting: seeds at io.tok_*[0..n) act as won entries
 //            pack(cost, 0); closes under `cutoff`; writes the merged frontier.
 // ===========================================================================
@@ -811,35 +937,37 @@ expand_kernel(GraphDev g, Params p, LaneWs L, UttDesc io, int n, int mode, doubl
     extern __shared__ double s_acrow[];
     const int tid = threadIdx.x;
     if (tid == 0) {
-        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.err = sm.err_frame = 0;
+        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = sm.err = sm.err_frame = 0;
         sm.err_aux = 0;
+        sm.fpar = 0;
+        sm.round_id = __ldcg(L.round_ctr);
+        sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
     for (int b = tid; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
     __syncthreads();
-    Lane ln(g, p, L, io, sm, s_acrow);
-    ln.round_id = __ldcg(L.round_ctr);
-    const double inf = __longlong_as_double(0x7FF0000000000000ll);
+    Lane<2> ln(g, p, L, io, sm, s_acrow);
     double cutoff = cutoff_in;
+    ln.par = 1;
     if (mode == 0) {
         ln.load_row(io.costs);
         __syncthreads();
         const double best = ln.emit(io.tok_state, io.tok_cost, n);
-        if (!(best < inf)) {
-            cutoff = inf;
+        if (!(best < inf_d())) {
+            cutoff = inf_d();
         } else {
             cutoff = __dadd_rn(best, p.beam);
-            ln.winners(io.tok_cost, cutoff, best);
+            ln.winners(cutoff, best);
         }
     } else {
         for (int i = tid; i < n; i += blockDim.x) {
             const unsigned s = __ldcg(io.tok_state + i);
             const double c = __ldcg(io.tok_cost + i);
-            __stcg(L.pack + s, pack_word(c, 0u));
-            __stcg(L.cost + s, c);
-            __stcg(L.pred + s, -1);
+            __stcg(&L.rec[s].pack, pack_word(c, 0u));
+            __stcg(&L.rec[s].cost[1], c);
+            __stcg(&L.rec[s].pred, -1);
             __stcg(L.touched + i, s);
-            __stcg(ln.fs + i, s);
-            __stcg(ln.fc + i, c);
+            __stcg(ln.fs() + i, s);
+            __stcg(ln.fc() + i, c);
         }
         __syncthreads();
         if (tid == 0) { sm.ntouched = n; sm.nfront = n; }
@@ -852,20 +980,20 @@ expand_kernel(GraphDev g, Params p, LaneWs L, UttDesc io, int n, int mode, doubl
     const int nt = sm.ntouched;
     for (int k = tid; k < nt; k += blockDim.x) {
         const unsigned v = __ldcg(L.touched + k);
-        const double c = __ldcg(L.cost + v);
+        const double c = __ldcg(&L.rec[v].cost[1]);
         if (c <= cutoff) {
             const int idx = agg_append(&sm.ntok);
             __stcg(io.tok_state + n + idx, v);
             __stcg(io.tok_cost + n + idx, c);
         }
+        __stcg(&L.rec[v].pack, SENT);
     }
     __syncthreads();
     if (tid == 0) {
         io.out_i[4] = sm.ntok;
         io.out_d[0] = cutoff;
-        __stcg(L.round_ctr, ln.round_id);
+        __stcg(L.round_ctr, sm.round_id);
     }
-    ln.reset();
 }
 
 // Fill helpers.
@@ -873,8 +1001,12 @@ __global__ void fill_f64(double *p, double v, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
 }
-__global__ void set_tokidx(int *tokidx, const unsigned *states, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) tokidx[states[i]] = i;
+// expand_emitting setup: the frontier's states carry (cost[0], tokidx) like a previous frame.
+__global__ void setup_tokens(StateRec *rec, const unsigned *states, const double *costs, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        rec[states[i]].cost[0] = costs[i];
+        rec[states[i]].tokidx = i;
+    }
 }
 
 }  // namespace lbk
