@@ -58,7 +58,8 @@ def parse_args(argv=None):
                    help="utterances per step per GPU (= decode lanes)")
     p.add_argument("--frames", type=int, default=300)
     p.add_argument("--lanes", type=int, default=0)
-    p.add_argument("--threads", type=int, default=0, help="threads per lane (CTA size)")
+    p.add_argument("--threads", type=int, default=0, help="threads per CTA of a lane")
+    p.add_argument("--ctas", type=int, default=0, help="CTAs (thread-block cluster size) per lane")
     p.add_argument("--states", type=int, default=5_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -221,7 +222,8 @@ def config_dict(args, note=""):
     d = {"workload": "C4: sequence-parallel batch on the C2 HCLG graph (1-best, beam 13, max-active 7000)",
          "graph": f"hclg_graph(seed=0, states={args.states}), 3000 pdfs, acyclic epsilon depth<=4",
          "utts_per_step_per_gpu": args.utts, "frames_per_utt": args.frames, "beam": 13.0,
-         "max_active": 7000, "lanes": args.lanes or args.utts, "threads_per_lane": args.threads or 1024,
+         "max_active": 7000, "lanes": args.lanes or "auto", "threads_per_cta": args.threads or 768,
+         "ctas_per_lane": args.ctas or 2,
          "l2": "flushed between steps (256 MiB write); graph 0.36 GB > L2"}
     if note:
         d["note"] = note
@@ -244,7 +246,7 @@ def main(argv=None):
     torch.cuda.set_device(dev)
     graph = synthetic.hclg_graph(0, num_states=args.states)
     cfg = lb.DecodeConfig(beam=13.0, max_active=7000, lanes=args.lanes, threads_per_lane=args.threads,
-                          device=dev)
+                          ctas_per_lane=args.ctas, device=dev)
     lb.device_graph(graph, dev)
     U, T = args.utts, args.frames
     pool = 2 * U

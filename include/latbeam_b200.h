@@ -47,7 +47,8 @@ typedef struct {
     int32_t want_lattice;         /* decode_utterance(want_lattice=...)  */
     int32_t collect_frame_packs;  /* keep per-frame token lists for readback */
     int32_t lanes;                /* concurrent utterances per launch (CTAs); 0 = auto */
-    int32_t threads_per_lane;     /* CTA size: 256/512/1024; 0 = auto     */
+    int32_t threads_per_lane;     /* CTA size: 256/512/768/1024; 0 = auto */
+    int32_t ctas_per_lane;        /* thread-block cluster size of a lane (1..4); 0 = auto */
 } lb_config;
 
 int32_t lb_version(void);
@@ -102,6 +103,10 @@ int lb_result_counters(const lb_result *r, int32_t utt, int64_t *counters);
  * number of kernel launches the call made. */
 int lb_result_timing(const lb_result *r, float *decode_ms, float *prune_ms, float *h2d_ms,
                      float *d2h_ms, int32_t *launches);
+/* Per-phase device time of the decode kernel summed over lanes (ms): emit, winners,
+ * max-active, epsilon, aggregate, lattice, frame turnover, frame0+final.  Zero unless
+ * the environment variable LB_PHASE_PROFILE=1 was set for the call (profiling aid). */
+int lb_result_phases(const lb_result *r, double *ms8);
 void lb_result_free(lb_result *r);
 
 /* Single-op surfaces (decoder.py:373-435): one frontier on device.

@@ -40,6 +40,7 @@ SIGNATURES = {
     "lb_result_counters": (C.c_int, [PV, C.c_int32, P64]),
     "lb_result_timing": (C.c_int, [PV, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                    C.POINTER(C.c_float), C.POINTER(C.c_float), P32]),
+    "lb_result_phases": (C.c_int, [PV, PD]),
     "lb_result_free": (None, [PV]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,
                                      P64, PD]),
@@ -52,7 +53,7 @@ class LbConfig(C.Structure):
                 ("max_active", C.c_int64), ("max_tokens_per_frame", C.c_int64),
                 ("max_lattice_arcs", C.c_int64), ("token_arena", C.c_int64),
                 ("want_lattice", C.c_int32), ("collect_frame_packs", C.c_int32),
-                ("lanes", C.c_int32), ("threads_per_lane", C.c_int32)]
+                ("lanes", C.c_int32), ("threads_per_lane", C.c_int32), ("ctas_per_lane", C.c_int32)]
 
 
 _lib = None

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -122,6 +123,7 @@ struct lb_result {
     std::vector<UttHost> utts;
     float t_decode = 0, t_prune = 0, t_h2d = 0, t_d2h = 0;
     int launches = 0;
+    double phase_ms[8] = {0};   // lane-summed phase times (LB_PHASE_PROFILE=1 only)
 };
 
 namespace {
@@ -313,8 +315,10 @@ int validate_cfg(const lb_config *c) {
     if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
     if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
     if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
-    if (c->threads_per_lane && (c->threads_per_lane % 32 || c->threads_per_lane > 1024 || c->threads_per_lane < 64))
-        return set_err(LB_USAGE, "threads_per_lane must be a multiple of 32 in [64, 1024]");
+    if (c->threads_per_lane != 0 && c->threads_per_lane != 256 && c->threads_per_lane != 512 &&
+        c->threads_per_lane != 768 && c->threads_per_lane != 1024)
+        return set_err(LB_USAGE, "threads_per_lane must be 256, 512, 768 or 1024");
+    if (c->ctas_per_lane < 0 || c->ctas_per_lane > 4) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 4]");
     return LB_OK;
 }
 
@@ -331,7 +335,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     tok_cap = std::min<int64_t>(tok_cap, (int64_t)1 << 31);
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
-    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 1024;
+    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
     // lanes: requested, else as many as fit a memory budget (<= 2 waves of SMs)
     const size_t per_lane = (size_t)S * (64 + (lat ? 8 : 0)) + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
                             (size_t)lat_cap * 28 + (size_t)path_cap * 4 + (size_t)(tmax + 2) * 16 + 256;
@@ -339,7 +343,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     CK(cudaMemGetInfo(&free_b, &total_b));
     const size_t reuse = (size_t)g->ws.lanes * per_lane;
     const size_t budget = (size_t)((double)(free_b + reuse) * 0.85);
-    int lanes = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, 2 * g->sms);
+    const int C = cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2;
+    int lanes = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / C));
     lanes = std::max(1, std::min(lanes, n > 0 ? n : 1));
     while (lanes > 1 && (size_t)lanes * per_lane > budget) lanes--;
     if ((size_t)lanes * per_lane > budget)
@@ -359,13 +364,27 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     p.collect_packs = packs;
     const size_t acrow_bytes = (size_t)D * 8;
     p.acrow_smem = acrow_bytes <= 160 * 1024;
+    p.prof = nullptr;
+    const char *pe = getenv("LB_PHASE_PROFILE");
+    unsigned long long *d_prof = nullptr;
+    if (pe && pe[0] == '1') {
+        CK(cudaMalloc((void **)&d_prof, 8 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st));
+        p.prof = d_prof;
+    }
     const size_t smem = p.acrow_smem ? acrow_bytes : 0;
-    // decode-lane variants: CTA size x batch width (all spill-free at their register budget)
-    void (*kern)(GraphDev, Params, const LaneWs *, const UttDesc *, int) = decode_kernel<1024, 2>;
-    if (threads == 768) kern = decode_kernel<768, 2>;
-    else if (threads == 512) kern = decode_kernel<512, 4>;
-    else if (threads == 256) kern = decode_kernel<256, 4>;
-    else if (threads != 1024) return set_err(LB_USAGE, "threads_per_lane must be 256, 512, 768 or 1024");
+    // decode-lane variants: CTA size x batch width x lattice x phase-profile
+    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, int);
+    const bool prof = p.prof != nullptr;
+#define LB_PICK(NT, U)                                                                     \
+    (lat ? (prof ? decode_kernel<NT, U, true, true> : decode_kernel<NT, U, true, false>) \
+         : (prof ? decode_kernel<NT, U, false, true> : decode_kernel<NT, U, false, false>))
+    KernT kern;
+    if (threads == 1024) kern = LB_PICK(1024, 2);
+    else if (threads == 768) kern = LB_PICK(768, 2);
+    else if (threads == 512) kern = LB_PICK(512, 4);
+    else return set_err(LB_USAGE, "threads_per_lane must be 512, 768 or 1024");
+#undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();
 
@@ -387,8 +406,21 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaMemcpyAsync(w.d_desc, desc.data(), nw * sizeof(UttDesc), cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(w.out_i, 0, 8 * sizeof(int) * nw, st));
         CK(cudaEventRecord(e0, st));
-        kern<<<nw, threads, smem, st>>>(gd, p, w.d_lanes, w.d_desc, nw);
-        CK(cudaGetLastError());
+        {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)(nw * C));
+            lc.blockDim = dim3((unsigned)threads);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)C;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc, nw));
+        }
         res->launches++;
         CK(cudaEventRecord(e1, st));
         if (lat) {
@@ -466,6 +498,12 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     cudaEventDestroy(e3);
+    if (d_prof) {
+        unsigned long long h[8];
+        CK(cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < 8; k++) res->phase_ms[k] = h[k] / 1e6;
+        cudaFree(d_prof);
+    }
     return LB_OK;
 }
 
@@ -733,6 +771,12 @@ int lb_result_timing(const lb_result *r, float *decode_ms, float *prune_ms, floa
     if (h2d_ms) *h2d_ms = r->t_h2d;
     if (d2h_ms) *d2h_ms = r->t_d2h;
     if (launches) *launches = r->launches;
+    return LB_OK;
+}
+
+int lb_result_phases(const lb_result *r, double *ms8) {
+    if (!r || !ms8) return set_err(LB_USAGE, "NULL argument");
+    std::memcpy(ms8, r->phase_ms, sizeof(r->phase_ms));
     return LB_OK;
 }
 

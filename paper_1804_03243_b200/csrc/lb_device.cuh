@@ -103,7 +103,14 @@ struct Params {
     int want_lattice;
     int collect_packs;
     int acrow_smem;
+    unsigned long long *prof;   // optional per-phase ns accumulators (LB_PHASE_PROFILE=1)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---- bit helpers ----
 __device__ __forceinline__ unsigned long long pack_word(double c, unsigned a) {

@@ -1,26 +1,29 @@
 // lb_kernels.cuh — the sm_100a decode-lane kernels.
 //
-// One CTA is one decode lane and owns one utterance of a wave (the paper's
-// sequence parallelism, as lanes instead of MPS processes).
-// A lane walks the utterance's frames in order; inside a frame the CTA runs the
-// phases below, separated by __syncthreads (no grid-wide sync, no host round
-// trip per frame).  Every per-state access of a phase lands in the state's one
-// 32-byte StateRec sector, and the hot loops are batched 4-wide so each thread
-// keeps 4 independent gathers / atomics in flight.
+// A decode lane is one thread-block CLUSTER (C CTAs, C = 1..4) that owns one
+// utterance of a wave (the paper's sequence parallelism, as
+// lanes instead of MPS processes).  The lane walks the utterance's frames in
+// order; inside a frame its C CTAs split every phase below and meet at cluster
+// barriers.  The lane's counters (touched / frontier / token / lattice list
+// lengths, error flag) live in the shared memory of the cluster's rank-0 CTA and
+// are updated through distributed shared memory, so no frame ever leaves the
+// GPU.  Fewer, wider lanes keep every lane's hot per-state records L2-resident
+// (SURVEY.md §7 step 7).  Hot loops are batched UNR-wide so every thread keeps
+// UNR independent gathers / atomics in flight.
 //
 //   emit      warp-cooperative expansion of the previous frame's tokens: the warp
 //             takes 32 tokens, prefix-scans their out-degrees with shuffles
 //             (Alg. 2 / static partition, scheduler.py:60-78) and walks the
-//             flattened arc range 128 arcs at a time (4 per lane), each lane
-//             binary-searching its owner token with shuffles; 16 B arc loads;
-//             one 64-bit atomicMin per candidate on the packed (cost, arc) word
-//             (Alg. 1, decoder.py:189-205); states seen for the first time
-//             (old == sentinel) go to the touched list with one shared atomic
-//             per warp.  The frame best is a block min over ALL candidates.
+//             flattened arc range 32*UNR arcs at a time, each lane binary-
+//             searching its owner token with shuffles; 16 B arc loads; one 64-bit
+//             atomicMin per candidate on the packed (cost, arc) word (Alg. 1,
+//             decoder.py:189-205); states seen for the first time (old ==
+//             sentinel) go to the touched list (one DSMEM atomic per warp).  The
+//             frame best is a cluster min over ALL candidates.
 //   winners   per touched state: the winner's f64 cost is recomputed from its
-//             arc and its source token's cost (the same operands in the same
-//             order => bit-identical to the offer) and the state is seeded if
-//             cost <= cutoff; max-active histogram.
+//             arc and its source token's cost (same operands, same order =>
+//             bit-identical to the offer); seed if cost <= cutoff; max-active
+//             histogram (per CTA, merged through DSMEM).
 //   epsilon   Jacobi rounds (reference.py:160-192): phase A offers pack words
 //             from snapshot costs, phase B lets the round's unique winning offer
 //             write the state's f64 cost / source.
@@ -31,57 +34,65 @@
 //             candidate <= cutoff and its destination was kept; epsilon arc live
 //             iff both ends kept and min-snapshot(src) + w <= cutoff.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "lb_device.cuh"
 
 namespace lbk {
 
+namespace cgx = cooperative_groups;
 
 struct Smem {
+    // lane-wide (meaningful in the rank-0 CTA only)
     int ntouched, nfront, nnext, ntok, nlat, nfix, err, err_frame;
     long long err_aux;
-    double cutoff;
-    unsigned round_id;      // epsilon round tag (persistent per lane)
-    int fpar;               // which frontier buffer is current
     unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
+    // per CTA
+    unsigned round_id;      // epsilon round tag (identical in every CTA of the lane)
+    int fpar;               // current frontier buffer (identical in every CTA)
+    double red0;
+    int ired0;
     double red[32];
-    long long lred[32];
     int ired[32];
     int hist[NBINS];
 };
 
 __device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7FF0000000000000ll); }
 
-__device__ __forceinline__ double block_min(double v, Smem &sm) {
+// The cluster that runs one lane.
+struct Grp {
+    Smem *S;        // this CTA's shared state
+    Smem *M;        // rank-0 CTA's shared state (DSMEM)
+    int rank, C;
+    __device__ __forceinline__ void sync() const { cgx::this_cluster().sync(); }
+    __device__ __forceinline__ Smem *at(int q) const { return cgx::this_cluster().map_shared_rank(S, q); }
+    __device__ __forceinline__ int gtid() const { return rank * blockDim.x + threadIdx.x; }
+    __device__ __forceinline__ int gstride() const { return C * blockDim.x; }
+    __device__ __forceinline__ int gwarp() const { return rank * (blockDim.x >> 5) + (threadIdx.x >> 5); }
+    __device__ __forceinline__ int gnw() const { return C * (blockDim.x >> 5); }
+    __device__ __forceinline__ bool leader() const { return rank == 0 && threadIdx.x == 0; }
+};
+
+// Cluster-wide min; result on every thread of the lane.
+__device__ __forceinline__ double cl_min(double v, const Grp &G) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_min(v);
-    if (lane == 0) sm.red[warp] = v;
+    if (lane == 0) G.S->red[warp] = v;
     __syncthreads();
     if (warp == 0) {
-        double x = lane < nw ? sm.red[lane] : inf_d();
+        double x = lane < nw ? G.S->red[lane] : inf_d();
         x = warp_min(x);
-        if (lane == 0) sm.red[0] = x;
+        if (lane == 0) G.S->red0 = x;
     }
-    __syncthreads();
-    double r = sm.red[0];
-    __syncthreads();
+    G.sync();
+    double r = inf_d();
+    for (int q = 0; q < G.C; q++) r = fmin(r, G.at(q)->red0);
+    G.sync();
     return r;
 }
 
-template <typename T>
-__device__ __forceinline__ T block_sum(T v, Smem &sm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_sum(v);
-    if (lane == 0) sm.lred[warp] = (long long)v;
-    __syncthreads();
-    T r = 0;
-    if (threadIdx.x == 0)
-        for (int k = 0; k < nw; k++) r += (T)sm.lred[k];
-    __syncthreads();
-    return r;   // valid on thread 0
-}
-
-// (value, state) lexicographic min; returns on all threads.
-__device__ __forceinline__ void block_argmin(double &v, int &s, Smem &sm) {
+// Cluster-wide (value, state) lexicographic min; result on every thread.
+__device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -89,34 +100,40 @@ __device__ __forceinline__ void block_argmin(double &v, int &s, Smem &sm) {
         int os = __shfl_xor_sync(FULL, s, o);
         if (ov < v || (ov == v && os < s)) { v = ov; s = os; }
     }
-    if (lane == 0) { sm.red[warp] = v; sm.ired[warp] = s; }
+    if (lane == 0) { G.S->red[warp] = v; G.S->ired[warp] = s; }
     __syncthreads();
     if (warp == 0) {
-        double x = lane < nw ? sm.red[lane] : inf_d();
-        int y = lane < nw ? sm.ired[lane] : 0x7FFFFFFF;
+        double x = lane < nw ? G.S->red[lane] : inf_d();
+        int y = lane < nw ? G.S->ired[lane] : 0x7FFFFFFF;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             double ov = __shfl_xor_sync(FULL, x, o);
             int os = __shfl_xor_sync(FULL, y, o);
             if (ov < x || (ov == x && os < y)) { x = ov; y = os; }
         }
-        if (lane == 0) { sm.red[0] = x; sm.ired[0] = y; }
+        if (lane == 0) { G.S->red0 = x; G.S->ired0 = y; }
     }
-    __syncthreads();
-    v = sm.red[0];
-    s = sm.ired[0];
-    __syncthreads();
+    G.sync();
+    v = inf_d();
+    s = 0x7FFFFFFF;
+    for (int q = 0; q < G.C; q++) {
+        const Smem *R = G.at(q);
+        const double x = R->red0;
+        const int y = R->ired0;
+        if (x < v || (x == v && y < s)) { v = x; s = y; }
+    }
+    G.sync();
 }
 
 // Warp-cooperative load-balanced walk over every (token, out-arc) pair of a
-// token list, UNR arcs per lane per batch.  f(valid[], i[], arc[], cost[])
-// receives one batch (the per-slot arrays are fully unrolled registers).
+// token list, UNR arcs per lane per batch; warps of all CTAs of the lane share
+// the list.  f(valid[], i[], arc[], cost[]) receives one batch.
 template <int UNR, class F>
-__device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, const unsigned *ts,
-                                                           const double *tc, int n, unsigned &c_scan,
-                                                           F &&f) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int base = warp * 32; base < n; base += nw * 32) {
+__device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, const Grp &G,
+                                                           const unsigned *ts, const double *tc, int n,
+                                                           unsigned &c_scan, F &&f) {
+    const int lane = threadIdx.x & 31;
+    for (int base = G.gwarp() * 32; base < n; base += G.gnw() * 32) {
         const int i = base + lane;
         const bool valid = i < n;
         const unsigned s = valid ? __ldcg(ts + i) : 0u;
@@ -159,36 +176,35 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
     }
 }
 
-// Per-CTA decode state (block-uniform).  UNR = independent items per thread per batch.
+// Per-lane decode phases.  UNR = independent items per thread per batch.
 template <int UNR>
 struct Lane {
-    const GraphDev &g;
-    const Params &p;
+    const GraphDev &g;      // __grid_constant__ kernel parameters: referenced in place,
+    const Params &p;        // never copied to local memory
     const LaneWs &L;
     const UttDesc &io;
-    Smem &sm;
+    const Grp G;
     double *acrow;          // shared-memory row (when p.acrow_smem)
     const double *row;      // global row of the current frame
     int par;                // parity of the current frame (cost slot)
 
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
-                    Smem &sm_, double *acrow_)
-        : g(g_), p(p_), L(L_), io(io_), sm(sm_), acrow(acrow_), row(nullptr), par(0) {}
+                    const Grp &G_, double *acrow_)
+        : g(g_), p(p_), L(L_), io(io_), G(G_), acrow(acrow_), row(nullptr), par(0) {}
 
-    // current / next frontier buffers (block-uniform selector in shared memory)
-    __device__ __forceinline__ unsigned *fs() const { return sm.fpar ? L.fs1 : L.fs0; }
-    __device__ __forceinline__ unsigned *fsn() const { return sm.fpar ? L.fs0 : L.fs1; }
-    __device__ __forceinline__ double *fc() const { return sm.fpar ? L.fc1 : L.fc0; }
-    __device__ __forceinline__ double *fcn() const { return sm.fpar ? L.fc0 : L.fc1; }
+    __device__ __forceinline__ unsigned *fs() const { return G.S->fpar ? L.fs1 : L.fs0; }
+    __device__ __forceinline__ unsigned *fsn() const { return G.S->fpar ? L.fs0 : L.fs1; }
+    __device__ __forceinline__ double *fc() const { return G.S->fpar ? L.fc1 : L.fc0; }
+    __device__ __forceinline__ double *fcn() const { return G.S->fpar ? L.fc0 : L.fc1; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
         return p.acrow_smem ? acrow[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
     }
 
-    __device__ __forceinline__ void set_error(int code, int frame, long long aux) {
-        if (atomicCAS(&sm.err, 0, code) == 0) {
-            sm.err_frame = frame;
-            sm.err_aux = aux;
+    __device__ __forceinline__ void set_error(int code, int frame, long long aux) const {
+        if (atomicCAS(&G.M->err, 0, code) == 0) {
+            G.M->err_frame = frame;
+            G.M->err_aux = aux;
         }
     }
 
@@ -198,13 +214,14 @@ struct Lane {
             for (int d = threadIdx.x; d < p.D; d += blockDim.x) acrow[d] = __dmul_rn(__ldg(r + d), p.scale);
     }
 
-    // ---- emit: returns the block-wide best candidate ----
+    // ---- emit: returns the lane-wide best candidate ----
     __device__ double emit(const unsigned *pts, const double *ptc, int np) {
         double lbest = inf_d();
         StateRec *rec = L.rec;
         unsigned c_scan = 0, c_cand = 0;
-        for_each_token_arc_batched<UNR>(g, pts, ptc, np, c_scan,
-                                   [&](const bool *vv, const int *, const unsigned *aa, const double *cc) {
+        int *ntouched = &G.M->ntouched;
+        for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan,
+                                        [&](const bool *vv, const int *, const unsigned *aa, const double *cc) {
             int4 r[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++)
@@ -225,7 +242,7 @@ struct Lane {
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (em[u] && old[u] == SENT) {
-                    const int sl = agg_append(&sm.ntouched);
+                    const int sl = agg_append(ntouched);
                     __stcg(L.touched + sl, (unsigned)r[u].x);
                 }
             }
@@ -233,27 +250,29 @@ struct Lane {
         c_cand = warp_sum(c_cand);
         c_scan = warp_sum(c_scan);
         if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&sm.c_cand, (unsigned long long)c_cand);
-            atomicAdd(&sm.c_scan, (unsigned long long)c_scan);
+            atomicAdd(&G.M->c_cand, (unsigned long long)c_cand);
+            atomicAdd(&G.M->c_scan, (unsigned long long)c_scan);
         }
-        return block_min(lbest, sm);
+        return cl_min(lbest, G);
     }
 
     // ---- winners: f64 cost of every touched state; seed frontier; histogram ----
     __device__ void winners(double cutoff, double best) {
-        const int nt = sm.ntouched;
+        const int nt = G.M->ntouched;
         const bool hist = p.max_active > 0;
         const double width = __ddiv_rn(p.beam, (double)NBINS);
         const int pp = par ^ 1;
         StateRec *rec = L.rec;
         unsigned *fs = this->fs();
         double *fc = this->fc();
-        for (int k0 = threadIdx.x; k0 < nt; k0 += UNR * blockDim.x) {
+        int *nfront = &G.M->nfront;
+        const int stride = G.gstride();
+        for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
             unsigned v[UNR];
             bool ok[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
-                const int k = k0 + u * blockDim.x;
+                const int k = k0 + u * stride;
                 ok[u] = k < nt;
                 v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
             }
@@ -265,7 +284,7 @@ struct Lane {
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (ok[u]) {
-                    const int2 lo = __ldg(reinterpret_cast<const int2 *>(g.arcs + a[u]) + 0);
+                    const int2 lo = __ldg(reinterpret_cast<const int2 *>(g.arcs + a[u]));
                     il[u] = (unsigned)lo.y;
                     w[u] = __ldg(reinterpret_cast<const double *>(g.arcs + a[u]) + 1);
                     src[u] = __ldg(g.src + a[u]);
@@ -287,13 +306,13 @@ struct Lane {
                 __stcg(&rec[v[u]].cost[par], cand);
                 __stcg(&rec[v[u]].pred, (pi[u] << 1) | 1);
                 if (cand <= cutoff) {
-                    const int sl = agg_append(&sm.nfront);
+                    const int sl = agg_append(nfront);
                     __stcg(fs + sl, v[u]);
                     __stcg(fc + sl, cand);
                     if (hist) {
                         const double q = __ddiv_rn(__dsub_rn(cand, best), width);
                         const int bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
-                        atomicAdd(&sm.hist[bin], 1);
+                        atomicAdd(&G.S->hist[bin], 1);
                     }
                 }
             }
@@ -301,8 +320,9 @@ struct Lane {
     }
 
     // max-active cutoff: H = best + max(b*,1)*width, b* = first
-    // bin whose inclusive running count exceeds max_active.  Warp 0 scans the
-    // 256-bin histogram (8 bins per lane); result is uniform.
+    // bin whose inclusive running count exceeds max_active.  Warp 0 of every CTA
+    // merges the lane's per-CTA histograms through DSMEM (8 bins per lane) and
+    // computes the same value; result is lane-uniform.  Called after a sync.
     __device__ double max_active_cutoff(double cutoff, double best) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         constexpr int PER = NBINS / 32;
@@ -310,10 +330,14 @@ struct Lane {
             int loc[PER];
             int sum = 0;
 #pragma unroll
-            for (int q = 0; q < PER; q++) {
-                loc[q] = sm.hist[lane * PER + q];
-                sum += loc[q];
+            for (int q = 0; q < PER; q++) loc[q] = 0;
+            for (int r = 0; r < G.C; r++) {
+                const Smem *R = G.at(r);
+#pragma unroll
+                for (int q = 0; q < PER; q++) loc[q] += R->hist[lane * PER + q];
             }
+#pragma unroll
+            for (int q = 0; q < PER; q++) sum += loc[q];
             int incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -335,28 +359,27 @@ struct Lane {
                 const double h = __dadd_rn(best, __dmul_rn((double)(bstar < 1 ? 1 : bstar), width));
                 c2 = h < cutoff ? h : cutoff;
             }
-            if (lane == 0) sm.cutoff = c2;
+            if (lane == 0) G.S->red0 = c2;
         }
         __syncthreads();
-        const double r = sm.cutoff;
-        __syncthreads();
+        const double r = G.S->red0;
+        G.sync();
         return r;
     }
 
-    // called by one thread between barriers
-    __device__ __forceinline__ void swap_frontier() { sm.fpar ^= 1; }
-
     // Keep frontier entries with cost <= cutoff (after a max-active tightening).
     __device__ void filter_frontier(double cutoff) {
-        const int nf = sm.nfront;
+        const int nf = G.M->nfront;
         unsigned *fs = this->fs(), *fsn = this->fsn();
         double *fc = this->fc(), *fcn = this->fcn();
-        for (int k0 = threadIdx.x; k0 < nf; k0 += UNR * blockDim.x) {
+        int *nnext = &G.M->nnext;
+        const int stride = G.gstride();
+        for (int k0 = G.gtid(); k0 < nf; k0 += UNR * stride) {
             double c[UNR];
             unsigned s[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
-                const int k = k0 + u * blockDim.x;
+                const int k = k0 + u * stride;
                 if (k < nf) {
                     c[u] = __ldcg(fc + k);
                     s[u] = __ldcg(fs + k);
@@ -367,40 +390,45 @@ struct Lane {
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (c[u] <= cutoff) {
-                    const int sl = agg_append(&sm.nnext);
+                    const int sl = agg_append(nnext);
                     __stcg(fsn + sl, s[u]);
                     __stcg(fcn + sl, c[u]);
                 }
             }
         }
-        __syncthreads();
+        G.sync();
+        const int nn = G.M->nnext;
+        G.sync();
         if (threadIdx.x == 0) {
-            sm.nfront = sm.nnext;
-            sm.nnext = 0;
-            swap_frontier();
+            if (G.rank == 0) {
+                G.M->nfront = nn;
+                G.M->nnext = 0;
+            }
+            G.S->fpar ^= 1;
         }
-        __syncthreads();
+        G.sync();
     }
 
     // ---- epsilon closure under a fixed cutoff (Jacobi rounds) ----
     __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
         StateRec *rec = L.rec;
+        const int stride = G.gstride();
         long long rounds = 0;
         for (;;) {
-            const int nf = sm.nfront;
+            const int nf = G.M->nfront;
             if (nf == 0) return true;
             if (++rounds > (long long)g.S + 1) {
-                if (threadIdx.x == 0) set_error(E_INT_EPS_ROUNDS, frame, 0);
-                __syncthreads();
+                if (G.leader()) set_error(E_INT_EPS_ROUNDS, frame, 0);
+                G.sync();
                 return false;
             }
-            const unsigned round_id = sm.round_id + 1;
+            const unsigned round_id = G.S->round_id + 1;
             unsigned *fs = this->fs(), *fsn = this->fsn();
             double *fc = this->fc(), *fcn = this->fcn();
             unsigned c_escan = 0, c_ecand = 0;
             // phase A: offers from snapshot costs
-            for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+            for (int k = G.gtid(); k < nf; k += stride) {
                 const unsigned u = __ldcg(fs + k);
                 const double cu = __ldcg(fc + k);
                 if (LAT) {
@@ -418,11 +446,11 @@ struct Lane {
                     const unsigned long long word = pack_word(cand, (unsigned)r.y);
                     const unsigned long long old = atomicMin(&rec[v].pack, word);
                     if (old == SENT) {
-                        const int sl = agg_append(&sm.ntouched);
+                        const int sl = agg_append(&G.M->ntouched);
                         __stcg(L.touched + sl, v);
                     }
                     if (old > word && atomicExch(L.tag + v, round_id) != round_id) {
-                        const int sl = agg_append(&sm.nnext);
+                        const int sl = agg_append(&G.M->nnext);
                         __stcg(fsn + sl, v);
                     }
                 }
@@ -430,12 +458,12 @@ struct Lane {
             c_escan = warp_sum(c_escan);
             c_ecand = warp_sum(c_ecand);
             if ((threadIdx.x & 31) == 0) {
-                atomicAdd(&sm.c_escan, (unsigned long long)c_escan);
-                atomicAdd(&sm.c_ecand, (unsigned long long)c_ecand);
+                atomicAdd(&G.M->c_escan, (unsigned long long)c_escan);
+                atomicAdd(&G.M->c_ecand, (unsigned long long)c_ecand);
             }
-            __syncthreads();
+            G.sync();
             // phase B: the round's unique winning offer writes cost / source
-            for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+            for (int k = G.gtid(); k < nf; k += stride) {
                 const unsigned u = __ldcg(fs + k);
                 const double cu = __ldcg(fc + k);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
@@ -451,34 +479,38 @@ struct Lane {
                     }
                 }
             }
-            __syncthreads();
-            const int nn = sm.nnext;
-            for (int k = threadIdx.x; k < nn; k += blockDim.x)
+            G.sync();
+            const int nn = G.M->nnext;
+            for (int k = G.gtid(); k < nn; k += stride)
                 __stcg(fcn + k, __ldcg(&rec[__ldcg(fsn + k)].cost[par]));
-            __syncthreads();
+            G.sync();
             if (threadIdx.x == 0) {
-                sm.c_front += nf;
-                sm.round_id = round_id;
-                sm.nfront = nn;
-                sm.nnext = 0;
-                swap_frontier();
+                if (G.rank == 0) {
+                    G.M->c_front += nf;
+                    G.M->nfront = nn;
+                    G.M->nnext = 0;
+                }
+                G.S->round_id = round_id;
+                G.S->fpar ^= 1;
             }
-            __syncthreads();
+            G.sync();
         }
     }
 
     // ---- aggregate + reset: frame token list at io.tok_*[tb ...]; returns count or -1 ----
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = sm.ntouched;
+        const int nt = G.M->ntouched;
         const long long room = io.tok_cap - tb;
         StateRec *rec = L.rec;
         unsigned *fix = fsn();  // scratch: tokens whose predecessor is an epsilon source state
-        for (int k0 = threadIdx.x; k0 < nt; k0 += UNR * blockDim.x) {
+        int *ntok = &G.M->ntok, *nfix = &G.M->nfix;
+        const int stride = G.gstride();
+        for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
             unsigned v[UNR];
             bool ok[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
-                const int k = k0 + u * blockDim.x;
+                const int k = k0 + u * stride;
                 ok[u] = k < nt;
                 v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
             }
@@ -499,7 +531,7 @@ struct Lane {
                 const bool init = frame == 0 && (int)v[u] == g.start;
                 const double c = init ? 0.0 : cs[u];
                 if (init || c <= cutoff) {
-                    const int idx = agg_append(&sm.ntok);
+                    const int idx = agg_append(ntok);
                     if (idx < room) {
                         const long long o = tb + idx;
                         __stcg(io.tok_state + o, v[u]);
@@ -509,7 +541,7 @@ struct Lane {
                         if (p.collect_packs) __stcg(io.tok_pack + o, pk[u]);
                         __stcg(&rec[v[u]].tokidx, idx);
                         if (!init && (pr[u] & 1) == 0) {
-                            const int f = agg_append(&sm.nfix);
+                            const int f = agg_append(nfix);
                             __stcg(fix + f, (unsigned)idx);
                         }
                     }
@@ -517,20 +549,18 @@ struct Lane {
                 __stcg(&rec[v[u]].pack, SENT);
             }
         }
-        __syncthreads();
-        const int n = sm.ntok;
-        if (n == 0) {
-            if (threadIdx.x == 0) set_error(E_DEAD_NO_TOKENS, frame, 0);
-        } else if ((long long)n > p.max_tokens) {
-            if (threadIdx.x == 0) set_error(E_CAP_TOKENS, frame, n);
-        } else if ((long long)n > room) {
-            if (threadIdx.x == 0) set_error(E_CAP_ARENA, frame, tb + n);
+        G.sync();
+        const int n = G.M->ntok;
+        if (G.leader()) {
+            if (n == 0) set_error(E_DEAD_NO_TOKENS, frame, 0);
+            else if ((long long)n > p.max_tokens) set_error(E_CAP_TOKENS, frame, n);
+            else if ((long long)n > room) set_error(E_CAP_ARENA, frame, tb + n);
         }
-        __syncthreads();
-        if (sm.err) return -1;
+        G.sync();
+        if (G.M->err) return -1;
         // epsilon predecessors: source state -> token index of this frame
-        const int nfx = sm.nfix;
-        for (int q = threadIdx.x; q < nfx; q += blockDim.x) {
+        const int nfx = G.M->nfix;
+        for (int q = G.gtid(); q < nfx; q += stride) {
             const long long o = tb + (long long)__ldcg(fix + q);
             const int u = __ldcg(io.tok_pred + o) >> 1;
             const int pi = __ldcg(&rec[u].tokidx);
@@ -538,12 +568,12 @@ struct Lane {
                 set_error(E_INT_EPS_PRED, frame, u);
             __stcg(io.tok_pred + o, pi << 1);
         }
-        __syncthreads();
-        return sm.err ? -1 : n;
+        G.sync();
+        return G.M->err ? -1 : n;
     }
 
     __device__ __forceinline__ void lat_push(int arc, int from, int to, long long lb) {
-        const int sl = agg_append(&sm.nlat);
+        const int sl = agg_append(&G.M->nlat);
         const long long gs = lb + sl;
         if (gs < io.lat_cap) {
             __stcg(io.lat_arc + gs, arc);
@@ -562,8 +592,8 @@ struct Lane {
                             long long lb) {
         if (frame > 0) {
             unsigned dummy = 0;
-            for_each_token_arc_batched<UNR>(g, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
-                                       [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
+            for_each_token_arc_batched<UNR>(g, G, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
+                                            [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
 #pragma unroll
                 for (int u = 0; u < UNR; u++) {
                     if (!vv[u]) continue;
@@ -578,7 +608,7 @@ struct Lane {
         }
         if (g.has_eps) {
             const double inf = inf_d();
-            for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            for (int j = G.gtid(); j < n; j += G.gstride()) {
                 const unsigned u = __ldcg(io.tok_state + tb + j);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
                 const double ms = __ldcg(L.minsnap + u);
@@ -591,31 +621,30 @@ struct Lane {
                 }
             }
         }
-        __syncthreads();
-        const int nl = sm.nlat;
-        if (lb + nl > io.lat_cap) {
-            if (threadIdx.x == 0) set_error(E_CAP_LATTICE, frame, lb + nl);
-        }
-        __syncthreads();
-        return sm.err == 0;
+        G.sync();
+        const int nl = G.M->nlat;
+        if (G.leader() && lb + nl > io.lat_cap) set_error(E_CAP_LATTICE, frame, lb + nl);
+        G.sync();
+        return G.M->err == 0;
     }
 
     // ---- per-frame counter reset (state words were reset in aggregate) ----
     __device__ void next_frame() {
-        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = 0;
+        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) G.S->hist[b] = 0;
+        G.sync();
+        if (G.leader()) {
+            Smem *M = G.M;
+            M->ntouched = M->nfront = M->nnext = M->ntok = M->nlat = M->nfix = 0;
         }
-        __syncthreads();
+        G.sync();
     }
 
     // ---- error path: O(touched) reset of every state word this frame touched ----
     __device__ void reset_touched() {
-        __syncthreads();
-        const int nt = sm.ntouched;
+        G.sync();
+        const int nt = G.M->ntouched;
         const double inf = inf_d();
-        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+        for (int k = G.gtid(); k < nt; k += G.gstride()) {
             const unsigned v = __ldcg(L.touched + k);
             __stcg(&L.rec[v].pack, SENT);
             if (p.want_lattice) __stcg(L.minsnap + v, inf);
@@ -624,38 +653,59 @@ struct Lane {
     }
 };
 
-// ===========================================================================
-// Full-utterance decode: one CTA per utterance of the wave.
-// ===========================================================================
-template <int NT, int UNR>
-__global__ void __launch_bounds__(NT, 1)
-decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts,
-              int n_utts) {
-    __shared__ Smem sm;
-    extern __shared__ double s_acrow[];
-    if ((int)blockIdx.x >= n_utts) return;
-    const LaneWs &L = lanes[blockIdx.x];
-    const UttDesc &io = utts[blockIdx.x];
-    const int tid = threadIdx.x;
-    if (tid == 0) {
+__device__ __forceinline__ void init_smem(Smem &sm, unsigned round_ctr) {
+    if (threadIdx.x == 0) {
         sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = sm.err = sm.err_frame = 0;
         sm.err_aux = 0;
         sm.fpar = 0;
-        sm.round_id = __ldcg(L.round_ctr);
+        sm.round_id = round_ctr;
         sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
-    for (int b = tid; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
-    __syncthreads();
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
+}
 
-    Lane<UNR> ln(g, p, L, io, sm, s_acrow);
+// ===========================================================================
+// Full-utterance decode: one cluster (lane) per utterance of the wave.
+// ===========================================================================
+template <int NT, int UNR, bool LAT, bool PROF>
+__global__ void __launch_bounds__(NT, 1)
+decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
+              const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts, int n_utts) {
+    __shared__ Smem sm;
+    extern __shared__ double s_acrow[];
+    cgx::cluster_group cl = cgx::this_cluster();
+    Grp G;
+    G.C = (int)cl.num_blocks();
+    G.rank = (int)cl.block_rank();
+    G.S = &sm;
+    G.M = cl.map_shared_rank(&sm, 0);
+    const int u_idx = blockIdx.x / G.C;      // uniform across the cluster
+    if (u_idx >= n_utts) return;
+    const LaneWs &L = lanes[u_idx];
+    const UttDesc &io = utts[u_idx];
+    init_smem(sm, __ldcg(L.round_ctr));
+    G.sync();
+
+    Lane<UNR> ln(g, p, L, io, G, s_acrow);
     const int T = io.T;
     const double inf = inf_d();
     long long tb = 0, lb = 0;
     int ntok = 0, tdone = 0;
 
+    // optional phase profile: leader accumulates globaltimer deltas per phase
+    unsigned long long t_last = 0;
+    auto mark = [&](int ph) {
+        if (PROF && G.leader()) {
+            const unsigned long long t = gtimer();
+            if (ph >= 0) atomicAdd(p.prof + ph, t - t_last);
+            t_last = t;
+        }
+    };
+    mark(-1);
+
     // ---- frame 0 (decoder.py:510-523): start token, epsilon closure ----
     ln.par = 0;
-    if (tid == 0) {
+    if (G.leader()) {
         __stcg(&L.rec[g.start].pack, pack_word(0.0, 0u));
         __stcg(&L.rec[g.start].cost[0], 0.0);
         __stcg(&L.rec[g.start].pred, -1);
@@ -667,7 +717,7 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         io.tok_base[0] = 0;
         if (p.want_lattice) io.lat_base[0] = 0;
     }
-    __syncthreads();
+    G.sync();
     double cutoff = __dadd_rn(0.0, p.beam);
     bool ok = ln.epsilon(cutoff, 0);
     bool reset_done = false;
@@ -676,72 +726,81 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         reset_done = true;
         ok = ntok > 0;
     }
-    if (ok && p.want_lattice) {
+    if (LAT && ok) {
         ok = ln.lattice(cutoff, 0, 0, 0, tb, ntok, lb);
-        lb += sm.nlat;
+        lb += G.M->nlat;
     }
-    if (tid == 0) {
+    if (G.leader()) {
         io.tok_base[1] = tb + (ok ? ntok : 0);
         if (p.want_lattice) io.lat_base[1] = lb;
     }
     if (reset_done) ln.next_frame(); else ln.reset_touched();
+    mark(7);
 
     for (int t = 1; ok && t <= T; t++) {
         const long long tbp = tb;
         const int np = ntok;
         tb += ntok;
-        if (tid == 0) sm.c_tok += np;
+        if (G.leader()) sm.c_tok += np;
         ln.par = t & 1;
         reset_done = false;
         ln.load_row(io.costs + (long long)(t - 1) * p.D);
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np);
+        mark(0);
         if (!(best < inf)) {
-            if (tid == 0) ln.set_error(E_DEAD_NO_CAND, t, 0);
+            if (G.leader()) ln.set_error(E_DEAD_NO_CAND, t, 0);
             ok = false;
             break;
         }
         cutoff = __dadd_rn(best, p.beam);
         ln.winners(cutoff, best);
-        __syncthreads();
-        if (sm.nfront == 0) {
-            if (tid == 0) ln.set_error(E_DEAD_NO_TOKENS, t, 0);
+        G.sync();
+        mark(1);
+        const int nf = G.M->nfront;
+        if (nf == 0) {
+            if (G.leader()) ln.set_error(E_DEAD_NO_TOKENS, t, 0);
             ok = false;
             break;
         }
-        if (p.max_active > 0 && sm.nfront > p.max_active) {
+        if (p.max_active > 0 && nf > p.max_active) {
             const double c2 = ln.max_active_cutoff(cutoff, best);
             if (c2 < cutoff) {
                 cutoff = c2;
                 ln.filter_frontier(cutoff);
             }
         }
+        mark(2);
         if (g.has_eps) {
             ok = ln.epsilon(cutoff, t);
             if (!ok) break;
         }
+        mark(3);
         ntok = ln.aggregate(cutoff, t, tb);
+        mark(4);
         reset_done = true;
         if (ntok < 0) { ok = false; break; }
-        if (tid == 0) sm.c_next += ntok;
-        if (p.want_lattice) {
+        if (G.leader()) sm.c_next += ntok;
+        if (LAT) {
             ok = ln.lattice(cutoff, t, tbp, np, tb, ntok, lb);
-            lb += sm.nlat;
+            lb += G.M->nlat;
         }
-        if (tid == 0) {
+        mark(5);
+        if (G.leader()) {
             io.tok_base[t + 1] = tb + ntok;
             if (p.want_lattice) io.lat_base[t + 1] = lb;
         }
         ln.next_frame();
+        mark(6);
         tdone = t;
     }
     if (!ok) {
         if (reset_done) ln.next_frame(); else ln.reset_touched();
     }
-    __syncthreads();
+    G.sync();
 
     // ---- counters ----
-    if (tid == 0) {
+    if (G.leader()) {
         io.out_c[0] = (long long)sm.c_tok;
         io.out_c[1] = (long long)sm.c_scan;
         io.out_c[2] = (long long)sm.c_cand;
@@ -753,30 +812,32 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         __stcg(L.round_ctr, sm.round_id);
         io.out_i[5] = tdone;
     }
-    if (!ok || sm.err) {
-        if (tid == 0) {
-            io.out_i[0] = sm.err ? sm.err : E_INT_INIT;
+    const int err = G.M->err;
+    if (!ok || err) {
+        if (G.leader()) {
+            io.out_i[0] = err ? err : E_INT_INIT;
             io.out_i[1] = sm.err_frame;
             io.out_d[2] = (double)sm.err_aux;
         }
+        G.sync();
         return;
     }
 
     // ---- final selection (decoder.py:578-586): argmin, ties -> smallest state ----
     double bt = inf, bc = inf;
     int st = 0x7FFFFFFF, sc = 0x7FFFFFFF;
-    for (int j = tid; j < ntok; j += blockDim.x) {
+    for (int j = G.gtid(); j < ntok; j += G.gstride()) {
         const unsigned s = __ldcg(io.tok_state + tb + j);
         const double c = __ldcg(io.tok_cost + tb + j);
         const double tot = __dadd_rn(c, __ldg(g.fin + s));
         if (tot < bt || (tot == bt && (int)s < st)) { bt = tot; st = (int)s; }
         if (c < bc || (c == bc && (int)s < sc)) { bc = c; sc = (int)s; }
     }
-    block_argmin(bt, st, sm);
-    block_argmin(bc, sc, sm);
+    cl_argmin(bt, st, G);
+    cl_argmin(bc, sc, G);
     const bool partial = !(bt < inf);
     const int bstate = partial ? sc : st;
-    if (tid == 0) {
+    if (G.leader()) {
         const double total = partial ? bc : bt;
         const int bidx = __ldcg(&L.rec[bstate].tokidx);
         io.out_i[2] = partial;
@@ -784,7 +845,7 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
         io.out_d[0] = total;
         io.out_d[1] = total;
         // ---- backtrace (decoder.py:614-641), bounded ----
-        int f = T, i = bidx, hops = 0, err = 0;
+        int f = T, i = bidx, hops = 0, e = 0;
         long long steps = 0;
         const long long limit = tb + ntok + 1;
         for (;;) {
@@ -792,14 +853,14 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
             const int a = __ldcg(io.tok_arc + base + i);
             const int pr = __ldcg(io.tok_pred + base + i);
             if (a < 0) {
-                if (f != 0) err = E_INT_INIT;
+                if (f != 0) e = E_INT_INIT;
                 break;
             }
-            if (hops >= io.path_cap) { err = E_CAP_PATH; break; }
+            if (hops >= io.path_cap) { e = E_CAP_PATH; break; }
             io.path[hops++] = a;
             i = pr >> 1;
             if (pr & 1) f--;
-            if (++steps > limit) { err = E_INT_BACKTRACE; break; }
+            if (++steps > limit) { e = E_INT_BACKTRACE; break; }
         }
         for (int k = 0; k < hops / 2; k++) {
             const int x = io.path[k];
@@ -807,9 +868,11 @@ decode_kernel(GraphDev g, Params p, const LaneWs *__restrict__ lanes, const UttD
             io.path[hops - 1 - k] = x;
         }
         io.out_i[4] = hops;
-        io.out_i[0] = err;
-        io.out_i[1] = err ? f : 0;
+        io.out_i[0] = e;
+        io.out_i[1] = e ? f : 0;
     }
+    mark(7);
+    G.sync();   // keep rank 0's shared memory alive until every CTA is done with it
 }
 
 // ===========================================================================
@@ -924,7 +987,7 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
 }
 
 // ===========================================================================
-// Single-op surfaces (decoder.py:373-435), one CTA.
+// Single-op surfaces (decoder.py:373-435), one CTA (a cluster of one).
 //   mode 0 = expand_emitting: tokens at io.tok_*[0..n), whose states carry
 //            (cost[0], tokidx) from setup_tokens; acrow (scaled) at io.costs;
 //            writes winners <= cutoff to io.tok_state/tok_cost[n ...].
@@ -932,20 +995,20 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
 //            pack(cost, 0); closes under `cutoff`; writes the merged frontier.
 // ===========================================================================
 __global__ void __launch_bounds__(1024, 1)
-expand_kernel(GraphDev g, Params p, LaneWs L, UttDesc io, int n, int mode, double cutoff_in) {
+expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
+              const __grid_constant__ LaneWs L, const __grid_constant__ UttDesc io, int n, int mode,
+              double cutoff_in) {
     __shared__ Smem sm;
     extern __shared__ double s_acrow[];
+    Grp G;
+    G.C = 1;
+    G.rank = 0;
+    G.S = &sm;
+    G.M = cgx::this_cluster().map_shared_rank(&sm, 0);
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = sm.err = sm.err_frame = 0;
-        sm.err_aux = 0;
-        sm.fpar = 0;
-        sm.round_id = __ldcg(L.round_ctr);
-        sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
-    }
-    for (int b = tid; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
+    init_smem(sm, __ldcg(L.round_ctr));
     __syncthreads();
-    Lane<2> ln(g, p, L, io, sm, s_acrow);
+    Lane<2> ln(g, p, L, io, G, s_acrow);
     double cutoff = cutoff_in;
     ln.par = 1;
     if (mode == 0) {

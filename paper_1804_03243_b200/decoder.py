@@ -44,7 +44,8 @@ class DecodeConfig:
     Added: `max_active` (0 = off, the reference behaviour; histogram cutoff,
     DESIGN.md §3), `token_arena` (tokens kept per utterance over all frames,
     0 = auto), `lanes` (utterances in flight per launch, 0 = auto),
-    `threads_per_lane` (CTA size, 0 = 1024), `device` (CUDA ordinal).
+    `threads_per_lane` (CTA size, 0 = 1024), `ctas_per_lane` (thread-block
+    cluster size of a lane, 0 = auto), `device` (CUDA ordinal).
     """
 
     beam: float = 14.0
@@ -61,6 +62,7 @@ class DecodeConfig:
     token_arena: int = 0
     lanes: int = 0
     threads_per_lane: int = 0
+    ctas_per_lane: int = 0
     device: int = 0
 
     def validate(self) -> None:
@@ -77,18 +79,21 @@ class DecodeConfig:
         if self.scheduler not in _SCHEDULERS:
             raise UsageError(f"unknown scheduler {self.scheduler!r}; choose one of "
                              f"{', '.join(_SCHEDULERS)}")
-        for name in ("max_active", "token_arena", "lanes", "threads_per_lane", "device"):
+        for name in ("max_active", "token_arena", "lanes", "threads_per_lane", "ctas_per_lane",
+                     "device"):
             if int(getattr(self, name)) < 0:
                 raise UsageError(f"{name} must be >= 0")
-        t = int(self.threads_per_lane)
-        if t and (t % 32 or not 64 <= t <= 1024):
-            raise UsageError("threads_per_lane must be a multiple of 32 in [64, 1024]")
+        if int(self.threads_per_lane) not in (0, 256, 512, 768, 1024):
+            raise UsageError("threads_per_lane must be 256, 512, 768 or 1024")
+        if not 0 <= int(self.ctas_per_lane) <= 4:
+            raise UsageError("ctas_per_lane must be in [0, 4]")
 
     def to_c(self, want_lattice: bool, collect_frame_packs: bool) -> LbConfig:
         return LbConfig(float(self.beam), float(self.lattice_beam), float(self.acoustic_scale),
                         int(self.max_active), int(self.max_tokens_per_frame),
                         int(self.max_lattice_arcs), int(self.token_arena), int(bool(want_lattice)),
-                        int(bool(collect_frame_packs)), int(self.lanes), int(self.threads_per_lane))
+                        int(bool(collect_frame_packs)), int(self.lanes), int(self.threads_per_lane),
+                        int(self.ctas_per_lane))
 
 
 @dataclass

@@ -54,6 +54,11 @@ def decode_batch_resident(wfst, tensors, config: DecodeConfig | None = None, str
             L.lb_result_path(res, u, ptr(path, P32))
             out.append({"status": st.value, "total_cost": tc.value, "partial": bool(part.value),
                         "path": path, "counters": cnt.copy()})
-        return out, result_timing(res)
+        tm = result_timing(res)
+        ph = np.zeros(8)
+        L.lb_result_phases(res, ptr(ph, PD))
+        tm["phases_ms"] = dict(zip(("emit", "winners", "max_active", "epsilon", "aggregate", "lattice",
+                                    "turnover", "frame0_final"), ph.tolist()))
+        return out, tm
     finally:
         L.lb_result_free(res)
