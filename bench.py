@@ -254,7 +254,8 @@ def main(argv=None):
     host = {s: np.ascontiguousarray(synthetic.hclg_matrix(s, num_frames=T).costs) for s in seeds}
     resident = {s: torch.from_numpy(a).to(f"cuda:{dev}") for s, a in host.items()}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)     # the decode kernels and the timing events share it
+    torch.cuda.set_stream(stream)
 
     def step_resident(k):
         outs, tm = decode_batch_resident(graph, [resident[s] for s in shard_seeds(dist.rank, k, U, pool)],

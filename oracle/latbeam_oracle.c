@@ -32,6 +32,7 @@
 #define SENT 0xFFFFFFFFFFFFFFFFull
 #define MAX_ACTIVE_BINS 256
 #define CONVERGE_TOL 1e-9
+#define MAX_ACTIVE_BEAM_DELTA 0.5   /* Kaldi's beam_delta (adaptive beam after max-active) */
 
 /* ---- packing (packing.py:37-61; kernels.py:51-67) ---- */
 static inline uint64_t enc32(double c) {
@@ -543,6 +544,7 @@ static int decode_ws(ws_t *w, const lbo_graph *g, const double *costs, int32_t T
     int rc = 0;
     double *seedc = NULL;
     int64_t seedcap = 0;
+    double beam_eff = cfg->beam;   /* adaptive beam; == beam when max_active == 0 */
     VPUSH(r.toff, 0);
     VPUSH(r.loff, 0);
 
@@ -595,7 +597,7 @@ static int decode_ws(ws_t *w, const lbo_graph *g, const double *costs, int32_t T
             rc = fail(out, LBO_DECODE_FAILURE, NULL, "beam search died at frame %d: no emitting candidates", t);
             goto done;
         }
-        cutoff = best + cfg->beam;
+        cutoff = best + beam_eff;
         /* seeds = winners under the cutoff (decoder.py:540; _winners :314-327) */
         int64_t ns = 0;
         if (w->ntouched > seedcap) { seedcap = w->ntouched; seedc = realloc(seedc, (size_t)seedcap * 8); }
@@ -609,11 +611,16 @@ static int decode_ws(ws_t *w, const lbo_graph *g, const double *costs, int32_t T
         }
         double c2 = max_active_cutoff(seedc, ns, best, cfg->beam, cfg->max_active, cutoff);
         if (c2 < cutoff) {
+            /* max-active bound: next frame's beam adapts (Kaldi GetCutoff's adaptive_beam) */
+            double be = (c2 - best) + MAX_ACTIVE_BEAM_DELTA;
+            beam_eff = be < cfg->beam ? be : cfg->beam;
             cutoff = c2;
             int64_t m = 0;
             for (int64_t k = 0; k < ns; k++)
                 if (seedc[k] <= cutoff) w->fs[m++] = w->fs[k];
             ns = m;
+        } else {
+            beam_eff = cfg->beam;
         }
         qsort(w->fs, (size_t)ns, 4, cmp_i32);
         for (int64_t k = 0; k < ns; k++) w->fc[k] = w->cost[w->fs[k]];

@@ -63,6 +63,7 @@ struct Workspace {
     // lane scratch
     StateRec *rec = nullptr;
     double *minsnap = nullptr, *fc0 = nullptr, *fc1 = nullptr;
+    uint2 *fe0 = nullptr, *fe1 = nullptr;
     unsigned *tag = nullptr, *touched = nullptr, *fs0 = nullptr, *fs1 = nullptr, *round_ctr = nullptr;
     // slots
     unsigned *tok_state = nullptr;
@@ -92,6 +93,7 @@ struct lb_graph {
     int sms = 148;
     int4 *arcs = nullptr;
     unsigned *src = nullptr, *ol = nullptr, *off = nullptr, *eoff = nullptr;
+    uint2 *rng = nullptr, *erng = nullptr;
     int4 *eps = nullptr;
     double *fin = nullptr;
     int64_t bytes = 0;
@@ -108,6 +110,8 @@ struct lb_graph {
         g.src = src;
         g.ol = ol;
         g.off = off;
+        g.rng = rng;
+        g.erng = erng;
         g.eoff = eoff;
         g.eps = eps;
         g.fin = fin;
@@ -156,6 +160,8 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
     CK(A(&w.touched, S * nl));
     CK(A(&w.fs0, S * nl));
     CK(A(&w.fs1, S * nl));
+    CK(A(&w.fe0, S * nl));
+    CK(A(&w.fe1, S * nl));
     CK(A(&w.round_ctr, nl));
     const size_t tc = (size_t)tok_cap, lc = (size_t)std::max<int64_t>(lat_cap, 1);
     CK(A(&w.tok_state, tc * nl));
@@ -198,6 +204,8 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
         x.fs1 = w.fs1 + l * S;
         x.fc0 = w.fc0 + l * S;
         x.fc1 = w.fc1 + l * S;
+        x.fe0 = w.fe0 + l * S;
+        x.fe1 = w.fe1 + l * S;
         x.round_ctr = w.round_ctr + l;
     }
     CK(cudaMemcpyAsync(w.d_lanes, hl.data(), nl * sizeof(LaneWs), cudaMemcpyHostToDevice, g->stream));
@@ -337,7 +345,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
     // lanes: requested, else as many as fit a memory budget (<= 2 waves of SMs)
-    const size_t per_lane = (size_t)S * (64 + (lat ? 8 : 0)) + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
+    const size_t per_lane = (size_t)S * (80 + (lat ? 8 : 0)) + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
                             (size_t)lat_cap * 28 + (size_t)path_cap * 4 + (size_t)(tmax + 2) * 16 + 256;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -583,6 +591,8 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     CK(dalloc(&g->src, A));
     CK(dalloc(&g->ol, A));
     CK(dalloc(&g->off, S + 1));
+    CK(dalloc(&g->rng, S));
+    CK(dalloc(&g->erng, S));
     CK(dalloc(&g->eoff, S + 1));
     CK(dalloc(&g->eps, g->E));
     CK(dalloc(&g->fin, S));
@@ -590,10 +600,17 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     CK(cudaMemcpy(g->src, hsrc.data(), 4 * A, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->ol, hol.data(), 4 * A, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->off, hoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
+    {
+        std::vector<uint2> hr((size_t)S);
+        for (int64_t s = 0; s < S; s++) hr[s] = make_uint2(hoff[s], hoff[s + 1]);
+        CK(cudaMemcpy(g->rng, hr.data(), sizeof(uint2) * S, cudaMemcpyHostToDevice));
+        for (int64_t s = 0; s < S; s++) hr[s] = make_uint2(heoff[s], heoff[s + 1]);
+        CK(cudaMemcpy(g->erng, hr.data(), sizeof(uint2) * S, cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(g->eoff, heoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
     if (g->E) CK(cudaMemcpy(g->eps, heps.data(), sizeof(int4) * g->E, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->fin, fin, 8 * S, cudaMemcpyHostToDevice));
-    g->bytes = A * 16 + A * 8 + (S + 1) * 8 + g->E * 16 + S * 8;
+    g->bytes = A * 16 + A * 8 + (S + 1) * 8 + 2 * S * 8 + g->E * 16 + S * 8;
     *out = g.release();
     return LB_OK;
 }
@@ -606,6 +623,8 @@ int lb_graph_destroy(lb_graph *g) {
     cudaFree(g->src);
     cudaFree(g->ol);
     cudaFree(g->off);
+    cudaFree(g->rng);
+    cudaFree(g->erng);
     cudaFree(g->eoff);
     cudaFree(g->eps);
     cudaFree(g->fin);

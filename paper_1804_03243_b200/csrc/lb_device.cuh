@@ -16,6 +16,7 @@ constexpr unsigned long long SENT = 0xFFFFFFFFFFFFFFFFull;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int NBINS = 256;              // max-active histogram bins
 constexpr double CONVERGE_TOL = 1e-9;   // lattice.py:36
+constexpr double MAX_ACTIVE_BEAM_DELTA = 0.5;   // Kaldi's beam_delta
 
 // ---- error codes written per utterance (host turns them into messages) ----
 enum : int {
@@ -41,7 +42,9 @@ struct GraphDev {
     const unsigned *src;
     const unsigned *ol;
     const unsigned *off;    // [S+1]
+    const uint2 *rng;       // [S] {first arc, end arc}: one 8-byte request per token
     const unsigned *eoff;   // [S+1] epsilon CSR offsets
+    const uint2 *erng;      // [S] {first, end} epsilon record of a state (one 8-byte request)
     const int4 *eps;        // epsilon records {dst, arc, w_lo, w_hi}
     const double *fin;      // final cost, +inf = non-final
     int S;
@@ -66,8 +69,9 @@ struct LaneWs {
     double *minsnap;        // min frontier snapshot cost this frame (lattice eps rule)
     unsigned *tag;          // epsilon round tag
     unsigned *touched;
-    unsigned *fs0, *fs1;
-    double *fc0, *fc1;
+    unsigned *fs0, *fs1;    // epsilon frontier: state,
+    double *fc0, *fc1;      //   snapshot cost,
+    uint2 *fe0, *fe1;       //   epsilon record range
     unsigned *round_ctr;    // persistent per-lane round counter
 };
 
@@ -143,6 +147,28 @@ __device__ __forceinline__ RecView load_rec(const StateRec *r) {
     v.pred = (int)(unsigned)(b.y & 0xFFFFFFFFull);
     v.tokidx = (int)(unsigned)(b.y >> 32);
     return v;
+}
+
+// One 32-byte request for a whole state record (sm_100 256-bit LDG/STG, L2 only).
+__device__ __forceinline__ RecView load_rec32(const StateRec *r) {
+    unsigned long long x0, x1, x2, x3;
+    asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(r) : "memory");
+    RecView v;
+    v.pack = x0;
+    v.cost0 = __longlong_as_double((long long)x1);
+    v.cost1 = __longlong_as_double((long long)x2);
+    v.pred = (int)(unsigned)(x3 & 0xFFFFFFFFull);
+    v.tokidx = (int)(unsigned)(x3 >> 32);
+    return v;
+}
+__device__ __forceinline__ void store_rec32(StateRec *r, unsigned long long pack, double c0, double c1,
+                                            int pred, int tokidx) {
+    const unsigned long long x3 = (unsigned long long)(unsigned)pred | ((unsigned long long)(unsigned)tokidx << 32);
+    asm volatile("st.global.cg.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(r), "l"(pack),
+                 "l"((unsigned long long)__double_as_longlong(c0)), "l"((unsigned long long)__double_as_longlong(c1)),
+                 "l"(x3)
+                 : "memory");
 }
 
 __device__ __forceinline__ void load_arc(const int4 *arcs, unsigned a, unsigned &dst, unsigned &il,

@@ -42,19 +42,25 @@ namespace lbk {
 
 namespace cgx = cooperative_groups;
 
+// Shared state of a lane.  Lane-wide fields are authoritative in the rank-0 CTA
+// (reached through DSMEM); they are double-buffered by frame parity (and the
+// epsilon frontier length by round parity) so a frame needs no barrier just to
+// reset counters: the set for frame t+1 is cleared while frame t runs.
 struct Smem {
-    // lane-wide (meaningful in the rank-0 CTA only)
-    int ntouched, nfront, nnext, ntok, nlat, nfix, err, err_frame;
+    int ntouched[2], ntok[2], nfix[2], nlat[2];
+    int nfr[3];                    // epsilon frontier lengths (round mod 3)
+    int nseed[2];                  // seeds (winners <= cutoff) per frame parity
+    unsigned long long best[2];    // order-preserving f64 frame best (frame parity)
+    int err, err_frame;
     long long err_aux;
     unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
     // per CTA
-    unsigned round_id;      // epsilon round tag (identical in every CTA of the lane)
-    int fpar;               // current frontier buffer (identical in every CTA)
+    unsigned round_id;             // epsilon round tag (identical in every CTA of the lane)
     double red0;
     int ired0;
     double red[32];
     int ired[32];
-    int hist[NBINS];
+    int hist[2][NBINS];            // max-active histogram (frame parity)
 };
 
 __device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7FF0000000000000ll); }
@@ -72,24 +78,6 @@ struct Grp {
     __device__ __forceinline__ int gnw() const { return C * (blockDim.x >> 5); }
     __device__ __forceinline__ bool leader() const { return rank == 0 && threadIdx.x == 0; }
 };
-
-// Cluster-wide min; result on every thread of the lane.
-__device__ __forceinline__ double cl_min(double v, const Grp &G) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_min(v);
-    if (lane == 0) G.S->red[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        double x = lane < nw ? G.S->red[lane] : inf_d();
-        x = warp_min(x);
-        if (lane == 0) G.S->red0 = x;
-    }
-    G.sync();
-    double r = inf_d();
-    for (int q = 0; q < G.C; q++) r = fmin(r, G.at(q)->red0);
-    G.sync();
-    return r;
-}
 
 // Cluster-wide (value, state) lexicographic min; result on every thread.
 __device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
@@ -138,9 +126,9 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
         const bool valid = i < n;
         const unsigned s = valid ? __ldcg(ts + i) : 0u;
         const double c = valid ? __ldcg(tc + i) : 0.0;
-        const unsigned lo = valid ? __ldg(g.off + s) : 0u;
-        const unsigned hi = valid ? __ldg(g.off + s + 1) : 0u;
-        const int deg = (int)(hi - lo);
+        const uint2 rg = valid ? __ldg(g.rng + s) : make_uint2(0u, 0u);
+        const unsigned lo = rg.x;
+        const int deg = (int)(rg.y - rg.x);
         int incl = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -186,16 +174,15 @@ struct Lane {
     const Grp G;
     double *acrow;          // shared-memory row (when p.acrow_smem)
     const double *row;      // global row of the current frame
-    int par;                // parity of the current frame (cost slot)
+    int par;                // parity of the current frame (cost slot, counter set)
 
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
                     const Grp &G_, double *acrow_)
         : g(g_), p(p_), L(L_), io(io_), G(G_), acrow(acrow_), row(nullptr), par(0) {}
 
-    __device__ __forceinline__ unsigned *fs() const { return G.S->fpar ? L.fs1 : L.fs0; }
-    __device__ __forceinline__ unsigned *fsn() const { return G.S->fpar ? L.fs0 : L.fs1; }
-    __device__ __forceinline__ double *fc() const { return G.S->fpar ? L.fc1 : L.fc0; }
-    __device__ __forceinline__ double *fcn() const { return G.S->fpar ? L.fc0 : L.fc1; }
+    __device__ __forceinline__ unsigned *fsb(int r) const { return (r & 1) ? L.fs1 : L.fs0; }
+    __device__ __forceinline__ double *fcb(int r) const { return (r & 1) ? L.fc1 : L.fc0; }
+    __device__ __forceinline__ uint2 *feb(int r) const { return (r & 1) ? L.fe1 : L.fe0; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
         return p.acrow_smem ? acrow[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
@@ -214,29 +201,75 @@ struct Lane {
             for (int d = threadIdx.x; d < p.D; d += blockDim.x) acrow[d] = __dmul_rn(__ldg(r + d), p.scale);
     }
 
-    // ---- emit: returns the lane-wide best candidate ----
-    __device__ double emit(const unsigned *pts, const double *ptc, int np) {
+    // Clear the counter set of the NEXT frame (leader only; its last readers are done).
+    __device__ __forceinline__ void clear_next_counters() const {
+        if (G.leader()) {
+            Smem *M = G.M;
+            const int q = par ^ 1;
+            M->ntouched[q] = M->ntok[q] = M->nfix[q] = M->nlat[q] = M->nseed[q] = 0;
+        }
+        if (threadIdx.x == 0) G.S->best[par ^ 1] = SENT;   // per-CTA partial of the next frame
+        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) G.S->hist[par ^ 1][b] = 0;
+    }
+
+    // ---- emit: returns the lane-wide best candidate (one cluster barrier) ----
+    // Every candidate feeds the frame best, but a candidate whose float32 key is
+    // above the float32 key of a running upper bound of this frame's cutoff
+    // (running best + beam_eff) skips its atomic: it can neither be the best nor
+    // the winner of a state that survives the cutoff, and no epsilon offer (cost
+    // <= cutoff) can tie with it, so every kept state's winner is unchanged.
+    __device__ double emit(const unsigned *pts, const double *ptc, int np, double beam_eff) {
         double lbest = inf_d();
         StateRec *rec = L.rec;
         unsigned c_scan = 0, c_cand = 0;
-        int *ntouched = &G.M->ntouched;
+        int *ntouched = &G.M->ntouched[par];
+        unsigned long long *run = &G.S->best[par];
+        unsigned bound_key = 0xFFFFFFFFu;     // enc32 of the running cutoff bound
+        if (G.leader()) G.M->nfr[0] = G.M->nfr[1] = G.M->nfr[2] = 0;
         for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan,
                                         [&](const bool *vv, const int *, const unsigned *aa, const double *cc) {
             int4 r[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++)
                 if (vv[u]) r[u] = __ldg(g.arcs + aa[u]);
+            double cand[UNR];
+            double bmin = inf_d();
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                cand[u] = inf_d();
+                if (vv[u] && r[u].y != 0) {
+                    const double w = __hiloint2double(r[u].w, r[u].z);
+                    cand[u] = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r[u].y));
+                    bmin = fmin(bmin, cand[u]);
+                }
+            }
+            lbest = fmin(lbest, bmin);
+            // share the running best through the CTA (one shared atomic per warp batch)
+            bmin = warp_min(bmin);
+            unsigned long long rb = 0;
+            if ((threadIdx.x & 31) == 0) {
+                const unsigned long long e = enc64(bmin);
+                const unsigned long long o = atomicMin(run, e);
+                rb = o < e ? o : e;
+            }
+            rb = __shfl_sync(FULL, rb, 0);
+            const double rbest = dec64(rb);
+            if (rbest < inf_d()) {
+                const unsigned k = (unsigned)(pack_word(__dadd_rn(rbest, beam_eff), 0u) >> 32);
+                bound_key = k < bound_key ? k : bound_key;
+            }
             unsigned long long old[UNR];
             bool em[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
-                em[u] = vv[u] && r[u].y != 0;
+                em[u] = cand[u] < inf_d();
                 if (em[u]) {
-                    const double w = __hiloint2double(r[u].w, r[u].z);
-                    const double cand = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r[u].y));
-                    lbest = fmin(lbest, cand);
-                    old[u] = atomicMin(&rec[r[u].x].pack, pack_word(cand, aa[u]));
-                    c_cand++;
+                    const unsigned long long word = pack_word(cand[u], aa[u]);
+                    em[u] = (unsigned)(word >> 32) <= bound_key;
+                    if (em[u]) {
+                        old[u] = atomicMin(&rec[r[u].x].pack, word);
+                        c_cand++;
+                    }
                 }
             }
 #pragma unroll
@@ -247,25 +280,34 @@ struct Lane {
                 }
             }
         });
+        lbest = warp_min(lbest);
         c_cand = warp_sum(c_cand);
         c_scan = warp_sum(c_scan);
         if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&G.M->c_cand, (unsigned long long)c_cand);
-            atomicAdd(&G.M->c_scan, (unsigned long long)c_scan);
+            // CTA-local shared atomics; the lane-wide min is merged after the barrier
+            atomicMin(run, enc64(lbest));
+            atomicAdd(&G.S->c_cand, (unsigned long long)c_cand);
+            atomicAdd(&G.S->c_scan, (unsigned long long)c_scan);
         }
-        return cl_min(lbest, G);
+        G.sync();
+        unsigned long long b = SENT;
+        for (int q = 0; q < G.C; q++) {
+            const unsigned long long x = G.at(q)->best[par];
+            b = x < b ? x : b;
+        }
+        return dec64(b);
     }
 
-    // ---- winners: f64 cost of every touched state; seed frontier; histogram ----
+    // ---- winners: f64 cost of every touched state; seeds; epsilon frontier (round 0); histogram ----
     __device__ void winners(double cutoff, double best) {
-        const int nt = G.M->ntouched;
+        const int nt = G.M->ntouched[par];
         const bool hist = p.max_active > 0;
+        const bool eps = g.has_eps;
         const double width = __ddiv_rn(p.beam, (double)NBINS);
         const int pp = par ^ 1;
         StateRec *rec = L.rec;
-        unsigned *fs = this->fs();
-        double *fc = this->fc();
-        int *nfront = &G.M->nfront;
+        int *nfront = &G.M->nfr[0], *nseed = &G.M->nseed[par];
+        int *hst = G.S->hist[par];
         const int stride = G.gstride();
         for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
             unsigned v[UNR];
@@ -277,16 +319,18 @@ struct Lane {
                 v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
             }
             unsigned a[UNR];
+            uint2 er[UNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) a[u] = ok[u] ? (unsigned)__ldcg(&rec[v[u]].pack) : 0u;
-            unsigned il[UNR], src[UNR];
-            double w[UNR];
+            for (int u = 0; u < UNR; u++) {
+                a[u] = ok[u] ? (unsigned)__ldcg(&rec[v[u]].pack) : 0u;
+                er[u] = (ok[u] && eps) ? __ldg(g.erng + v[u]) : make_uint2(0u, 0u);
+            }
+            int4 ar[UNR];
+            unsigned src[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (ok[u]) {
-                    const int2 lo = __ldg(reinterpret_cast<const int2 *>(g.arcs + a[u]));
-                    il[u] = (unsigned)lo.y;
-                    w[u] = __ldg(reinterpret_cast<const double *>(g.arcs + a[u]) + 1);
+                    ar[u] = __ldg(g.arcs + a[u]);
                     src[u] = __ldg(g.src + a[u]);
                 }
             }
@@ -295,24 +339,30 @@ struct Lane {
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (ok[u]) {
-                    pc[u] = __ldcg(&rec[src[u]].cost[pp]);
-                    pi[u] = __ldcg(&rec[src[u]].tokidx);
+                    const RecView sr = load_rec32(&rec[src[u]]);
+                    pc[u] = sr.cost(pp);
+                    pi[u] = sr.tokidx;
                 }
             }
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (!ok[u]) continue;
-                const double cand = __dadd_rn(__dadd_rn(pc[u], w[u]), ac(il[u]));
+                const double w = __hiloint2double(ar[u].w, ar[u].z);
+                const double cand = __dadd_rn(__dadd_rn(pc[u], w), ac((unsigned)ar[u].y));
                 __stcg(&rec[v[u]].cost[par], cand);
                 __stcg(&rec[v[u]].pred, (pi[u] << 1) | 1);
                 if (cand <= cutoff) {
-                    const int sl = agg_append(nfront);
-                    __stcg(fs + sl, v[u]);
-                    __stcg(fc + sl, cand);
+                    agg_append(nseed);
+                    if (er[u].x < er[u].y) {      // only states with epsilon arcs enter the closure
+                        const int sl = agg_append(nfront);
+                        __stcg(L.fs0 + sl, v[u]);
+                        __stcg(L.fc0 + sl, cand);
+                        __stcg(L.fe0 + sl, er[u]);
+                    }
                     if (hist) {
                         const double q = __ddiv_rn(__dsub_rn(cand, best), width);
                         const int bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
-                        atomicAdd(&G.S->hist[bin], 1);
+                        atomicAdd(&hst[bin], 1);
                     }
                 }
             }
@@ -322,7 +372,8 @@ struct Lane {
     // max-active cutoff: H = best + max(b*,1)*width, b* = first
     // bin whose inclusive running count exceeds max_active.  Warp 0 of every CTA
     // merges the lane's per-CTA histograms through DSMEM (8 bins per lane) and
-    // computes the same value; result is lane-uniform.  Called after a sync.
+    // computes the same value, so no cluster barrier is needed.  Called after a
+    // cluster barrier that follows winners().
     __device__ double max_active_cutoff(double cutoff, double best) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         constexpr int PER = NBINS / 32;
@@ -334,7 +385,7 @@ struct Lane {
             for (int r = 0; r < G.C; r++) {
                 const Smem *R = G.at(r);
 #pragma unroll
-                for (int q = 0; q < PER; q++) loc[q] += R->hist[lane * PER + q];
+                for (int q = 0; q < PER; q++) loc[q] += R->hist[par][lane * PER + q];
             }
 #pragma unroll
             for (int q = 0; q < PER; q++) sum += loc[q];
@@ -363,147 +414,139 @@ struct Lane {
         }
         __syncthreads();
         const double r = G.S->red0;
-        G.sync();
+        __syncthreads();
         return r;
     }
 
-    // Keep frontier entries with cost <= cutoff (after a max-active tightening).
-    __device__ void filter_frontier(double cutoff) {
-        const int nf = G.M->nfront;
-        unsigned *fs = this->fs(), *fsn = this->fsn();
-        double *fc = this->fc(), *fcn = this->fcn();
-        int *nnext = &G.M->nnext;
+    // Keep the round-0 epsilon frontier entries with cost <= cutoff (after a
+    // max-active tightening): buffer 0 -> buffer 1 (count nfr[1]), one batched
+    // pass and one barrier; the epsilon closure then starts at round 1.
+    __device__ void filter_seeds(double cutoff) {
+        const int nf = G.M->nfr[0];
+        int *nout = &G.M->nfr[1];
         const int stride = G.gstride();
-        for (int k0 = G.gtid(); k0 < nf; k0 += UNR * stride) {
-            double c[UNR];
-            unsigned s[UNR];
+        for (int k0 = G.gtid(); k0 < nf; k0 += 4 * stride) {
+            double c[4];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
+            for (int u = 0; u < 4; u++) {
                 const int k = k0 + u * stride;
-                if (k < nf) {
-                    c[u] = __ldcg(fc + k);
-                    s[u] = __ldcg(fs + k);
-                } else {
-                    c[u] = inf_d();
-                }
+                c[u] = k < nf ? __ldcg(L.fc0 + k) : inf_d();
             }
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
+            for (int u = 0; u < 4; u++) {
                 if (c[u] <= cutoff) {
-                    const int sl = agg_append(nnext);
-                    __stcg(fsn + sl, s[u]);
-                    __stcg(fcn + sl, c[u]);
+                    const int k = k0 + u * stride;
+                    const int sl = agg_append(nout);
+                    __stcg(L.fs1 + sl, __ldcg(L.fs0 + k));
+                    __stcg(L.fc1 + sl, c[u]);
+                    __stcg(L.fe1 + sl, __ldcg(L.fe0 + k));
                 }
             }
-        }
-        G.sync();
-        const int nn = G.M->nnext;
-        G.sync();
-        if (threadIdx.x == 0) {
-            if (G.rank == 0) {
-                G.M->nfront = nn;
-                G.M->nnext = 0;
-            }
-            G.S->fpar ^= 1;
         }
         G.sync();
     }
 
-    // ---- epsilon closure under a fixed cutoff (Jacobi rounds) ----
-    __device__ bool epsilon(double cutoff, int frame) {
+    // ---- epsilon closure under a fixed cutoff: Jacobi rounds, two barriers each ----
+    // Round r reads frontier buffer (r&1) = (state, snapshot cost, epsilon range),
+    // count nfr[r%3].  Phase A: each entry parks its snapshot in its record's
+    // cost[par^1] slot (dead after winners), offers pack words, and tags improved
+    // states (the first tagger appends the state to the next frontier).  Phase B:
+    // for each improved state the winning arc is read from the pack; its f64 cost
+    // is recomputed from the source's parked snapshot (same operands => the
+    // winning offer's exact value) and written with the source as predecessor.
+    __device__ bool epsilon(double cutoff, int frame, int r0 = 0) {
         const bool LAT = p.want_lattice;
         StateRec *rec = L.rec;
         const int stride = G.gstride();
-        long long rounds = 0;
-        for (;;) {
-            const int nf = G.M->nfront;
-            if (nf == 0) return true;
-            if (++rounds > (long long)g.S + 1) {
+        const int pp = par ^ 1;
+        unsigned round_id = G.S->round_id;
+        unsigned c_escan = 0, c_ecand = 0, c_front = 0;
+        bool ok = true;
+        for (int r = r0;; r++) {
+            const int nf = G.M->nfr[r % 3];
+            if (nf == 0) break;
+            if (r > g.S + 1) {
                 if (G.leader()) set_error(E_INT_EPS_ROUNDS, frame, 0);
-                G.sync();
-                return false;
+                ok = false;
+                break;
             }
-            const unsigned round_id = G.S->round_id + 1;
-            unsigned *fs = this->fs(), *fsn = this->fsn();
-            double *fc = this->fc(), *fcn = this->fcn();
-            unsigned c_escan = 0, c_ecand = 0;
+            ++round_id;
+            const unsigned *fs = fsb(r);
+            const double *fc = fcb(r);
+            const uint2 *fe = feb(r);
+            unsigned *fsn = fsb(r + 1);
+            double *fcn = fcb(r + 1);
+            uint2 *fen = feb(r + 1);
+            int *nnext = &G.M->nfr[(r + 1) % 3];
+            if (G.leader()) G.M->nfr[(r + 2) % 3] = 0;   // read at round r-1's start, two barriers ago
             // phase A: offers from snapshot costs
             for (int k = G.gtid(); k < nf; k += stride) {
-                const unsigned u = __ldcg(fs + k);
                 const double cu = __ldcg(fc + k);
+                if (!(cu <= cutoff)) continue;
+                const unsigned u = __ldcg(fs + k);
+                const uint2 er = __ldcg(fe + k);
+                c_front++;
                 if (LAT) {
                     const double m = __ldcg(L.minsnap + u);
                     if (cu < m) __stcg(L.minsnap + u, cu);
                 }
-                const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                c_escan += e1 - e0;
-                for (unsigned e = e0; e < e1; ++e) {
-                    const int4 r = __ldg(g.eps + e);
-                    const double cand = __dadd_rn(cu, __hiloint2double(r.w, r.z));
+                __stcg(&rec[u].cost[pp], cu);
+                c_escan += er.y - er.x;
+                for (unsigned e = er.x; e < er.y; ++e) {
+                    const int4 rr = __ldg(g.eps + e);
+                    const double cand = __dadd_rn(cu, __hiloint2double(rr.w, rr.z));
                     if (!(cand <= cutoff)) continue;
                     c_ecand++;
-                    const unsigned v = (unsigned)r.x;
-                    const unsigned long long word = pack_word(cand, (unsigned)r.y);
+                    const unsigned v = (unsigned)rr.x;
+                    const unsigned long long word = pack_word(cand, (unsigned)rr.y);
                     const unsigned long long old = atomicMin(&rec[v].pack, word);
                     if (old == SENT) {
-                        const int sl = agg_append(&G.M->ntouched);
+                        const int sl = agg_append(&G.M->ntouched[par]);
                         __stcg(L.touched + sl, v);
                     }
                     if (old > word && atomicExch(L.tag + v, round_id) != round_id) {
-                        const int sl = agg_append(&G.M->nnext);
+                        const int sl = agg_append(nnext);
                         __stcg(fsn + sl, v);
                     }
                 }
             }
-            c_escan = warp_sum(c_escan);
-            c_ecand = warp_sum(c_ecand);
-            if ((threadIdx.x & 31) == 0) {
-                atomicAdd(&G.M->c_escan, (unsigned long long)c_escan);
-                atomicAdd(&G.M->c_ecand, (unsigned long long)c_ecand);
-            }
             G.sync();
-            // phase B: the round's unique winning offer writes cost / source
-            for (int k = G.gtid(); k < nf; k += stride) {
-                const unsigned u = __ldcg(fs + k);
-                const double cu = __ldcg(fc + k);
-                const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                for (unsigned e = e0; e < e1; ++e) {
-                    const int4 r = __ldg(g.eps + e);
-                    const double cand = __dadd_rn(cu, __hiloint2double(r.w, r.z));
-                    if (!(cand <= cutoff)) continue;
-                    const unsigned v = (unsigned)r.x;
-                    if (__ldcg(&rec[v].pack) == pack_word(cand, (unsigned)r.y) &&
-                        __ldcg(L.tag + v) == round_id) {
-                        __stcg(&rec[v].cost[par], cand);
-                        __stcg(&rec[v].pred, (int)(u << 1));
-                    }
-                }
-            }
-            G.sync();
-            const int nn = G.M->nnext;
-            for (int k = G.gtid(); k < nn; k += stride)
-                __stcg(fcn + k, __ldcg(&rec[__ldcg(fsn + k)].cost[par]));
-            G.sync();
-            if (threadIdx.x == 0) {
-                if (G.rank == 0) {
-                    G.M->c_front += nf;
-                    G.M->nfront = nn;
-                    G.M->nnext = 0;
-                }
-                G.S->round_id = round_id;
-                G.S->fpar ^= 1;
+            // phase B: improved states recover their round winner from the pack
+            const int nn = *nnext;
+            for (int k = G.gtid(); k < nn; k += stride) {
+                const unsigned v = __ldcg(fsn + k);
+                const unsigned a = (unsigned)__ldcg(&rec[v].pack);
+                const double w = __ldg(reinterpret_cast<const double *>(g.arcs + a) + 1);
+                const unsigned u = __ldg(g.src + a);
+                const uint2 er = __ldg(g.erng + v);
+                const double cand = __dadd_rn(__ldcg(&rec[u].cost[pp]), w);
+                __stcg(&rec[v].cost[par], cand);
+                __stcg(&rec[v].pred, (int)(u << 1));
+                __stcg(fcn + k, cand);
+                __stcg(fen + k, er);
             }
             G.sync();
         }
+        c_escan = warp_sum(c_escan);
+        c_ecand = warp_sum(c_ecand);
+        c_front = warp_sum(c_front);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&G.S->c_escan, (unsigned long long)c_escan);
+            atomicAdd(&G.S->c_ecand, (unsigned long long)c_ecand);
+            atomicAdd(&G.S->c_front, (unsigned long long)c_front);
+        }
+        if (threadIdx.x == 0) G.S->round_id = round_id;
+        if (!ok) G.sync();
+        return ok;
     }
 
     // ---- aggregate + reset: frame token list at io.tok_*[tb ...]; returns count or -1 ----
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = G.M->ntouched;
+        const int nt = G.M->ntouched[par];
         const long long room = io.tok_cap - tb;
         StateRec *rec = L.rec;
-        unsigned *fix = fsn();  // scratch: tokens whose predecessor is an epsilon source state
-        int *ntok = &G.M->ntok, *nfix = &G.M->nfix;
+        unsigned *fix = L.fs1;  // scratch: tokens whose predecessor is an epsilon source state
+        int *ntok = &G.M->ntok[par], *nfix = &G.M->nfix[par];
         const int stride = G.gstride();
         for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
             unsigned v[UNR];
@@ -514,66 +557,66 @@ struct Lane {
                 ok[u] = k < nt;
                 v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
             }
-            unsigned long long pk[UNR];
-            double cs[UNR];
-            int pr[UNR];
+            RecView r[UNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (ok[u]) {
-                    pk[u] = __ldcg(&rec[v[u]].pack);
-                    cs[u] = __ldcg(&rec[v[u]].cost[par]);
-                    pr[u] = __ldcg(&rec[v[u]].pred);
-                }
-            }
+            for (int u = 0; u < UNR; u++)
+                if (ok[u]) r[u] = load_rec32(&rec[v[u]]);
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 if (!ok[u]) continue;
                 const bool init = frame == 0 && (int)v[u] == g.start;
-                const double c = init ? 0.0 : cs[u];
+                const double c = init ? 0.0 : r[u].cost(par);
+                int tidx = r[u].tokidx;
                 if (init || c <= cutoff) {
                     const int idx = agg_append(ntok);
                     if (idx < room) {
                         const long long o = tb + idx;
                         __stcg(io.tok_state + o, v[u]);
                         __stcg(io.tok_cost + o, c);
-                        __stcg(io.tok_arc + o, init ? -1 : (int)(unsigned)pk[u]);
-                        __stcg(io.tok_pred + o, init ? -1 : pr[u]);
-                        if (p.collect_packs) __stcg(io.tok_pack + o, pk[u]);
-                        __stcg(&rec[v[u]].tokidx, idx);
-                        if (!init && (pr[u] & 1) == 0) {
+                        __stcg(io.tok_arc + o, init ? -1 : (int)(unsigned)r[u].pack);
+                        __stcg(io.tok_pred + o, init ? -1 : r[u].pred);
+                        if (p.collect_packs) __stcg(io.tok_pack + o, r[u].pack);
+                        tidx = idx;
+                        if (!init && (r[u].pred & 1) == 0) {
                             const int f = agg_append(nfix);
                             __stcg(fix + f, (unsigned)idx);
                         }
                     }
                 }
                 __stcg(&rec[v[u]].pack, SENT);
+                if (tidx != r[u].tokidx) __stcg(&rec[v[u]].tokidx, tidx);
             }
         }
         G.sync();
-        const int n = G.M->ntok;
-        if (G.leader()) {
-            if (n == 0) set_error(E_DEAD_NO_TOKENS, frame, 0);
-            else if ((long long)n > p.max_tokens) set_error(E_CAP_TOKENS, frame, n);
-            else if ((long long)n > room) set_error(E_CAP_ARENA, frame, tb + n);
+        const int n = G.M->ntok[par];
+        if (n == 0 || (long long)n > p.max_tokens || (long long)n > room) {
+            if (G.leader()) {
+                if (n == 0) set_error(E_DEAD_NO_TOKENS, frame, 0);
+                else if ((long long)n > p.max_tokens) set_error(E_CAP_TOKENS, frame, n);
+                else set_error(E_CAP_ARENA, frame, tb + n);
+            }
+            G.sync();
+            return -1;
         }
-        G.sync();
-        if (G.M->err) return -1;
         // epsilon predecessors: source state -> token index of this frame
-        const int nfx = G.M->nfix;
-        for (int q = G.gtid(); q < nfx; q += stride) {
-            const long long o = tb + (long long)__ldcg(fix + q);
-            const int u = __ldcg(io.tok_pred + o) >> 1;
-            const int pi = __ldcg(&rec[u].tokidx);
-            if (pi < 0 || pi >= n || __ldcg(io.tok_state + tb + pi) != (unsigned)u)
-                set_error(E_INT_EPS_PRED, frame, u);
-            __stcg(io.tok_pred + o, pi << 1);
+        const int nfx = G.M->nfix[par];
+        if (nfx > 0) {
+            for (int q = G.gtid(); q < nfx; q += stride) {
+                const long long o = tb + (long long)__ldcg(fix + q);
+                const int u = __ldcg(io.tok_pred + o) >> 1;
+                const int pi = __ldcg(&rec[u].tokidx);
+                if (pi < 0 || pi >= n || __ldcg(io.tok_state + tb + pi) != (unsigned)u)
+                    set_error(E_INT_EPS_PRED, frame, u);
+                __stcg(io.tok_pred + o, pi << 1);
+            }
+            G.sync();
+            if (G.M->err) return -1;
         }
-        G.sync();
-        return G.M->err ? -1 : n;
+        return n;
     }
 
     __device__ __forceinline__ void lat_push(int arc, int from, int to, long long lb) {
-        const int sl = agg_append(&G.M->nlat);
+        const int sl = agg_append(&G.M->nlat[par]);
         const long long gs = lb + sl;
         if (gs < io.lat_cap) {
             __stcg(io.lat_arc + gs, arc);
@@ -587,9 +630,9 @@ struct Lane {
         return j >= 0 && j < n && __ldcg(io.tok_state + tb + j) == v;
     }
 
-    // ---- lattice arcs of block `frame` (rule A.5); resets minsnap ----
-    __device__ bool lattice(double cutoff, int frame, long long tbp, int np, long long tb, int n,
-                            long long lb) {
+    // ---- lattice arcs of block `frame` (rule A.5); resets minsnap; returns arc count or -1 ----
+    __device__ int lattice(double cutoff, int frame, long long tbp, int np, long long tb, int n,
+                           long long lb) {
         if (frame > 0) {
             unsigned dummy = 0;
             for_each_token_arc_batched<UNR>(g, G, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
@@ -622,50 +665,48 @@ struct Lane {
             }
         }
         G.sync();
-        const int nl = G.M->nlat;
-        if (G.leader() && lb + nl > io.lat_cap) set_error(E_CAP_LATTICE, frame, lb + nl);
-        G.sync();
-        return G.M->err == 0;
-    }
-
-    // ---- per-frame counter reset (state words were reset in aggregate) ----
-    __device__ void next_frame() {
-        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) G.S->hist[b] = 0;
-        G.sync();
-        if (G.leader()) {
-            Smem *M = G.M;
-            M->ntouched = M->nfront = M->nnext = M->ntok = M->nlat = M->nfix = 0;
+        const int nl = G.M->nlat[par];
+        if (lb + nl > io.lat_cap) {
+            if (G.leader()) set_error(E_CAP_LATTICE, frame, lb + nl);
+            G.sync();
+            return -1;
         }
-        G.sync();
+        return nl;
     }
 
     // ---- error path: O(touched) reset of every state word this frame touched ----
     __device__ void reset_touched() {
         G.sync();
-        const int nt = G.M->ntouched;
+        const int nt = G.M->ntouched[par];
         const double inf = inf_d();
         for (int k = G.gtid(); k < nt; k += G.gstride()) {
             const unsigned v = __ldcg(L.touched + k);
             __stcg(&L.rec[v].pack, SENT);
             if (p.want_lattice) __stcg(L.minsnap + v, inf);
         }
-        next_frame();
+        G.sync();
     }
 };
 
 __device__ __forceinline__ void init_smem(Smem &sm, unsigned round_ctr) {
     if (threadIdx.x == 0) {
-        sm.ntouched = sm.nfront = sm.nnext = sm.ntok = sm.nlat = sm.nfix = sm.err = sm.err_frame = 0;
+        for (int q = 0; q < 2; q++) {
+            sm.ntouched[q] = sm.ntok[q] = sm.nfix[q] = sm.nlat[q] = sm.nseed[q] = 0;
+            sm.best[q] = SENT;
+        }
+        sm.nfr[0] = sm.nfr[1] = sm.nfr[2] = 0;
+        sm.err = sm.err_frame = 0;
         sm.err_aux = 0;
-        sm.fpar = 0;
         sm.round_id = round_ctr;
         sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
-    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) sm.hist[b] = 0;
+    for (int b = threadIdx.x; b < 2 * NBINS; b += blockDim.x) sm.hist[b / NBINS][b % NBINS] = 0;
 }
 
 // ===========================================================================
 // Full-utterance decode: one cluster (lane) per utterance of the wave.
+// Cluster barriers per frame: emit 1, winners 1, epsilon 2 per round,
+// aggregate 1-2, lattice 1.
 // ===========================================================================
 template <int NT, int UNR, bool LAT, bool PROF>
 __global__ void __launch_bounds__(NT, 1)
@@ -703,6 +744,8 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     };
     mark(-1);
 
+    double beam_eff = p.beam;   // adaptive beam; == beam without max-active
+
     // ---- frame 0 (decoder.py:510-523): start token, epsilon closure ----
     ln.par = 0;
     if (G.leader()) {
@@ -710,12 +753,13 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         __stcg(&L.rec[g.start].cost[0], 0.0);
         __stcg(&L.rec[g.start].pred, -1);
         __stcg(L.touched, (unsigned)g.start);
-        __stcg(ln.fs(), (unsigned)g.start);
-        __stcg(ln.fc(), 0.0);
-        sm.ntouched = 1;
-        sm.nfront = 1;
+        __stcg(L.fs0, (unsigned)g.start);
+        __stcg(L.fc0, 0.0);
+        __stcg(L.fe0, g.has_eps ? __ldg(g.erng + g.start) : make_uint2(0u, 0u));
+        sm.ntouched[0] = 1;
+        sm.nfr[0] = 1;
         io.tok_base[0] = 0;
-        if (p.want_lattice) io.lat_base[0] = 0;
+        if (LAT) io.lat_base[0] = 0;
     }
     G.sync();
     double cutoff = __dadd_rn(0.0, p.beam);
@@ -727,14 +771,15 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         ok = ntok > 0;
     }
     if (LAT && ok) {
-        ok = ln.lattice(cutoff, 0, 0, 0, tb, ntok, lb);
-        lb += G.M->nlat;
+        const int nl = ln.lattice(cutoff, 0, 0, 0, tb, ntok, lb);
+        ok = nl >= 0;
+        if (ok) lb += nl;
     }
     if (G.leader()) {
         io.tok_base[1] = tb + (ok ? ntok : 0);
-        if (p.want_lattice) io.lat_base[1] = lb;
+        if (LAT) io.lat_base[1] = lb;
     }
-    if (reset_done) ln.next_frame(); else ln.reset_touched();
+    if (!reset_done) ln.reset_touched();
     mark(7);
 
     for (int t = 1; ok && t <= T; t++) {
@@ -746,67 +791,89 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         reset_done = false;
         ln.load_row(io.costs + (long long)(t - 1) * p.D);
         __syncthreads();
-        const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np);
+        const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff);
+        ln.clear_next_counters();   // frame t-1's readers are past the emit barrier
         mark(0);
         if (!(best < inf)) {
             if (G.leader()) ln.set_error(E_DEAD_NO_CAND, t, 0);
             ok = false;
             break;
         }
-        cutoff = __dadd_rn(best, p.beam);
+        cutoff = __dadd_rn(best, beam_eff);
         ln.winners(cutoff, best);
         G.sync();
         mark(1);
-        const int nf = G.M->nfront;
+        const int nf = G.M->nseed[ln.par];
         if (nf == 0) {
             if (G.leader()) ln.set_error(E_DEAD_NO_TOKENS, t, 0);
             ok = false;
             break;
         }
+        int r0 = 0;
+        bool tightened = false;
         if (p.max_active > 0 && nf > p.max_active) {
             const double c2 = ln.max_active_cutoff(cutoff, best);
             if (c2 < cutoff) {
+                tightened = true;
                 cutoff = c2;
-                ln.filter_frontier(cutoff);
+                if (g.has_eps) {   // without epsilon arcs the seeds are never read again
+                    ln.filter_seeds(cutoff);
+                    r0 = 1;
+                }
             }
+        }
+        // Kaldi's adaptive beam: after a max-active tightening the next frame's beam
+        // is (cutoff - best) + beam_delta, capped at beam; otherwise the full beam.
+        if (tightened) {
+            const double be = __dadd_rn(__dsub_rn(cutoff, best), MAX_ACTIVE_BEAM_DELTA);
+            beam_eff = be < p.beam ? be : p.beam;
+        } else {
+            beam_eff = p.beam;
         }
         mark(2);
         if (g.has_eps) {
-            ok = ln.epsilon(cutoff, t);
+            ok = ln.epsilon(cutoff, t, r0);
             if (!ok) break;
         }
         mark(3);
         ntok = ln.aggregate(cutoff, t, tb);
-        mark(4);
         reset_done = true;
+        mark(4);
         if (ntok < 0) { ok = false; break; }
         if (G.leader()) sm.c_next += ntok;
         if (LAT) {
-            ok = ln.lattice(cutoff, t, tbp, np, tb, ntok, lb);
-            lb += G.M->nlat;
+            const int nl = ln.lattice(cutoff, t, tbp, np, tb, ntok, lb);
+            if (nl < 0) { ok = false; break; }
+            lb += nl;
         }
         mark(5);
         if (G.leader()) {
             io.tok_base[t + 1] = tb + ntok;
-            if (p.want_lattice) io.lat_base[t + 1] = lb;
+            if (LAT) io.lat_base[t + 1] = lb;
         }
-        ln.next_frame();
         mark(6);
         tdone = t;
     }
-    if (!ok) {
-        if (reset_done) ln.next_frame(); else ln.reset_touched();
-    }
+    if (!ok && !reset_done) ln.reset_touched();
     G.sync();
 
-    // ---- counters ----
+    // ---- counters: per-CTA partials merged through DSMEM ----
     if (G.leader()) {
+        unsigned long long cs = 0, cc = 0, cf = 0, ces = 0, cec = 0;
+        for (int q = 0; q < G.C; q++) {
+            const Smem *R = G.at(q);
+            cs += R->c_scan;
+            cc += R->c_cand;
+            cf += R->c_front;
+            ces += R->c_escan;
+            cec += R->c_ecand;
+        }
         io.out_c[0] = (long long)sm.c_tok;
-        io.out_c[1] = (long long)sm.c_scan;
-        io.out_c[2] = (long long)sm.c_cand;
-        io.out_c[3] = (long long)sm.c_front;
-        io.out_c[4] = (long long)sm.c_escan;
-        io.out_c[5] = (long long)sm.c_ecand;
+        io.out_c[1] = (long long)cs;
+        io.out_c[2] = (long long)cc;
+        io.out_c[3] = (long long)cf;
+        io.out_c[4] = (long long)ces;
+        io.out_c[5] = (long long)cec;
         io.out_c[6] = (long long)sm.c_next;
         io.out_c[7] = lb;
         __stcg(L.round_ctr, sm.round_id);
@@ -1014,7 +1081,7 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     if (mode == 0) {
         ln.load_row(io.costs);
         __syncthreads();
-        const double best = ln.emit(io.tok_state, io.tok_cost, n);
+        const double best = ln.emit(io.tok_state, io.tok_cost, n, p.beam);
         if (!(best < inf_d())) {
             cutoff = inf_d();
         } else {
@@ -1029,23 +1096,24 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
             __stcg(&L.rec[s].cost[1], c);
             __stcg(&L.rec[s].pred, -1);
             __stcg(L.touched + i, s);
-            __stcg(ln.fs() + i, s);
-            __stcg(ln.fc() + i, c);
+            __stcg(L.fs0 + i, s);
+            __stcg(L.fc0 + i, c);
+            __stcg(L.fe0 + i, g.has_eps ? __ldg(g.erng + s) : make_uint2(0u, 0u));
         }
         __syncthreads();
-        if (tid == 0) { sm.ntouched = n; sm.nfront = n; }
+        if (tid == 0) { sm.ntouched[1] = n; sm.nfr[0] = n; }
         __syncthreads();
         if (!ln.epsilon(cutoff, 0)) {
             if (tid == 0) io.out_i[0] = sm.err;
         }
     }
     __syncthreads();
-    const int nt = sm.ntouched;
+    const int nt = sm.ntouched[1];
     for (int k = tid; k < nt; k += blockDim.x) {
         const unsigned v = __ldcg(L.touched + k);
         const double c = __ldcg(&L.rec[v].cost[1]);
         if (c <= cutoff) {
-            const int idx = agg_append(&sm.ntok);
+            const int idx = agg_append(&sm.ntok[1]);
             __stcg(io.tok_state + n + idx, v);
             __stcg(io.tok_cost + n + idx, c);
         }
@@ -1053,7 +1121,7 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     }
     __syncthreads();
     if (tid == 0) {
-        io.out_i[4] = sm.ntok;
+        io.out_i[4] = sm.ntok[1];
         io.out_d[0] = cutoff;
         __stcg(L.round_ctr, sm.round_id);
     }

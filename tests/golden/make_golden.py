@@ -157,6 +157,8 @@ def max_active_decode(wfst, matrix, beam, max_active, lattice_beam=8.0):
     internals, with the max-active cutoff of DESIGN.md §3 inserted after the
     emitting pass.  No lattice (1-best + frame packs)."""
     nb = 256
+    beam_delta = 0.5           # Kaldi's adaptive-beam delta
+    beam_eff = beam
     cfg = latbeam.DecodeConfig(beam=beam, num_workers=1, max_lattice_arcs=2_000_000)
     ws = D._Workspace(wfst)
     store = LT.ShardedArcStore(cfg.max_lattice_arcs, 1)
@@ -175,8 +177,9 @@ def max_active_decode(wfst, matrix, beam, max_active, lattice_beam=8.0):
         ws.reset_frame()
         best = D._emit(ws, wfst, toks, acrow, beam, store, cfg, None, t, False)
         store.counts[:] = 0                      # staging not needed for 1-best
-        cutoff = best + beam
+        cutoff = best + beam_eff
         ss, sc, _ = D._winners(ws, cutoff, t)
+        tightened = False
         if max_active and len(ss) > max_active:
             width = beam / nb
             q = (sc - best) / width
@@ -184,9 +187,12 @@ def max_active_decode(wfst, matrix, beam, max_active, lattice_beam=8.0):
             cum = np.cumsum(np.bincount(b, minlength=nb))
             bstar = int(np.argmax(cum > max_active))
             h = best + float(max(bstar, 1)) * width
-            cutoff = min(cutoff, h)
-            keep = sc <= cutoff
-            ss, sc = ss[keep], sc[keep]
+            if h < cutoff:
+                tightened = True
+                cutoff = h
+                keep = sc <= cutoff
+                ss, sc = ss[keep], sc[keep]
+        beam_eff = min(beam, (cutoff - best) + beam_delta) if tightened else beam
         D._eps_fixpoint(ws, wfst, store, cutoff, t, ss, sc, False)
         store.counts[:] = 0
         toks = D._aggregate(ws, wfst, cutoff, t, None, cfg.max_tokens_per_frame)
