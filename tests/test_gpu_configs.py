@@ -1,0 +1,97 @@
+"""Parity at BASELINE.json's full config sizes (C1-C5), device vs the CPU oracle.
+
+Every config runs its real graph (SURVEY.md §8(d) generators, full size) and
+real-length utterances:
+
+* C1  uniform 10k x 5, 500 pdfs, beam 13, lattice beam 8: all 20 utterances x
+      300 frames 1-best bit-exact (cost + work counters), two of them with
+      per-frame packs and the full lattice.
+* C2  HCLG 5M states, beam 13, max-active 7000, 1-best: one 300-frame utterance,
+      per-frame (state, pack) maps bit-exact.
+* C3  C2 + lattice beam 8: one 300-frame utterance, lattice arc sets / extras.
+* C4  C2 graph, sequence-parallel batch: 64 utterances in one launch (64 lanes),
+      every total cost and work counter bit-exact vs the threaded oracle.
+* C5  HCLG 15M states / ~50M arcs with 1000 epsilon hubs and depth-8 epsilon
+      chains, beam 16, max-active 20000: one 300-frame utterance bit-exact.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1804_03243_b200 as lb
+from paper_1804_03243_b200 import synthetic
+
+from parity_helpers import check_pair, decode_both
+
+pytestmark = pytest.mark.gpu
+
+_GRAPHS: dict = {}
+
+
+def graph(name):
+    key = "C2" if name in ("C2", "C3", "C4") else name
+    if key not in _GRAPHS:
+        _GRAPHS[key] = synthetic.config_graph(key)
+    return _GRAPHS[key]
+
+
+def _counters(r):
+    """Work counters that are a pure function of the token lists: tokens expanded,
+    arcs scanned, tokens kept (the device skips hopeless atomics, so its candidate
+    and epsilon-offer counts are legitimately lower than the oracle's)."""
+    c = r.counters
+    return [c["n_tokens"], c["n_scan"], c["n_next"]]
+
+
+def test_c1_all_utterances(oracle_mod):
+    w = graph("C1")
+    d = synthetic.CONFIGS["C1"]["decode"]
+    mats = [synthetic.config_matrix("C1", u) for u in range(20)]
+    tc, st, cnt = oracle_mod.decode_batch_mt(w, mats, d["beam"])
+    res = lb.decode_batch(w, mats, lb.DecodeConfig(beam=d["beam"]), want_lattice=False)
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()
+    for r, c in zip(res, cnt):
+        assert _counters(r) == [c[0], c[1], c[6]]
+    for u in range(2):
+        got, ref = decode_both(w, mats[u], oracle_mod, d["beam"], d["lattice_beam"])
+        check_pair(got, ref, d["lattice_beam"])
+
+
+@pytest.mark.parametrize("name,want_lattice", [("C2", False), ("C3", True)])
+def test_c2_c3_full_utterance(oracle_mod, name, want_lattice):
+    w = graph(name)
+    d = synthetic.CONFIGS[name]["decode"]
+    m = synthetic.config_matrix(name, 0)
+    got, ref = decode_both(w, m, oracle_mod, d["beam"], d["lattice_beam"],
+                           max_active=d["max_active"], want_lattice=want_lattice)
+    check_pair(got, ref, d["lattice_beam"], want_lattice=want_lattice)
+    # max-active binds on this graph: the cap is reached on most frames
+    sizes = np.asarray([len(s) for s, _ in got.frame_packs[1:]])
+    assert np.median(sizes) >= 0.9 * d["max_active"], np.median(sizes)
+
+
+def test_c4_batch_of_64_lanes(oracle_mod):
+    w = graph("C4")
+    d = synthetic.CONFIGS["C4"]["decode"]
+    mats = [synthetic.config_matrix("C4", u) for u in range(64)]
+    tc, st, cnt = oracle_mod.decode_batch_mt(w, mats, d["beam"], max_active=d["max_active"])
+    res = lb.decode_batch(w, mats, lb.DecodeConfig(beam=d["beam"], max_active=d["max_active"],
+                                                   lanes=64), want_lattice=False)
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()
+    for r, c in zip(res, cnt):
+        assert _counters(r) == [c[0], c[1], c[6]]
+
+
+def test_c5_stress_utterance(oracle_mod):
+    w = graph("C5")
+    assert w.num_arcs > 45_000_000  # ~49.9M
+    d = synthetic.CONFIGS["C5"]["decode"]
+    m = synthetic.config_matrix("C5", 0)
+    got, ref = decode_both(w, m, oracle_mod, d["beam"], d["lattice_beam"],
+                           max_active=d["max_active"], want_lattice=False)
+    check_pair(got, ref, d["lattice_beam"], want_lattice=False)
+    assert ref.counters["eps_scan"] > 0
