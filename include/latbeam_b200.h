@@ -47,7 +47,7 @@ typedef struct {
     int32_t want_lattice;         /* decode_utterance(want_lattice=...)  */
     int32_t collect_frame_packs;  /* keep per-frame token lists for readback */
     int32_t lanes;                /* concurrent utterances per launch (CTAs); 0 = auto */
-    int32_t threads_per_lane;     /* CTA size: 256/512/768/1024; 0 = auto */
+    int32_t threads_per_lane;     /* CTA size: 512 or 768; 0 = auto (768) */
     int32_t ctas_per_lane;        /* thread-block cluster size of a lane (1..4); 0 = auto */
 } lb_config;
 
@@ -107,6 +107,11 @@ int lb_result_timing(const lb_result *r, float *decode_ms, float *prune_ms, floa
  * max-active, epsilon, aggregate, lattice, frame turnover, frame0+final.  Zero unless
  * the environment variable LB_PHASE_PROFILE=1 was set for the call (profiling aid). */
 int lb_result_phases(const lb_result *r, double *ms8);
+/* Same profiling run: per phase, the busy time of every warp up to its arrival at
+ * the phase's closing barrier, summed over warps (ms), and the number of
+ * warp-phase samples; busy/samples vs the lane phase time separates slow work
+ * from waiting on the slowest warp. */
+int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8);
 void lb_result_free(lb_result *r);
 
 /* Single-op surfaces (decoder.py:373-435): one frontier on device.

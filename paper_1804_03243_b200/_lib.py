@@ -41,6 +41,7 @@ SIGNATURES = {
     "lb_result_timing": (C.c_int, [PV, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                    C.POINTER(C.c_float), C.POINTER(C.c_float), P32]),
     "lb_result_phases": (C.c_int, [PV, PD]),
+    "lb_result_warp_phases": (C.c_int, [PV, PD, PD]),
     "lb_result_free": (None, [PV]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,
                                      P64, PD]),

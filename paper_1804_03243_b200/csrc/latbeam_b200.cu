@@ -53,18 +53,19 @@ struct UttHost {
     std::vector<uint64_t> packs;
 };
 
-// Per-graph reusable device workspace: lane scratch (O(S) per lane) and
-// utterance slots (token / lattice arenas).
+// Per-graph reusable device workspace: lane scratch (O(S) per lane, per-CTA
+// lists, candidate buffers) and utterance slots (token / lattice arenas).
 struct Workspace {
-    int lanes = 0;
-    int64_t S = 0, tok_cap = 0, lat_cap = 0;
+    int lanes = 0, C = 0;
+    int64_t S = 0, tok_cap = 0, lat_cap = 0, ccap = 0;
     int path_cap = 0, tmax = 0;
     bool packs = false, lat = false;
     // lane scratch
     StateRec *rec = nullptr;
-    double *minsnap = nullptr, *fc0 = nullptr, *fc1 = nullptr;
-    uint2 *fe0 = nullptr, *fe1 = nullptr;
-    unsigned *tag = nullptr, *touched = nullptr, *fs0 = nullptr, *fs1 = nullptr, *round_ctr = nullptr;
+    EpsWin *rpk = nullptr;
+    unsigned *tag = nullptr, *touched = nullptr, *fr = nullptr, *fix = nullptr, *round_ctr = nullptr;
+    int4 *cand = nullptr;
+    int *candi = nullptr;
     // slots
     unsigned *tok_state = nullptr;
     double *tok_cost = nullptr, *node_extra = nullptr, *lat_extra = nullptr, *tmp = nullptr;
@@ -84,12 +85,23 @@ struct Workspace {
     }
 };
 
+// Device bytes of one lane's scratch + slot (the lane-count budget).
+size_t lane_bytes(int64_t S, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap, int path_cap, int tmax,
+                  bool packs, bool lat) {
+    (void)lat;
+    return (size_t)S * (32 + 32 + 4 + (size_t)C * 16) + (size_t)C * ccap * 20 +
+           (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) + (size_t)lat_cap * 28 + (size_t)path_cap * 4 +
+           (size_t)(tmax + 2) * 16 + 256;
+}
+
 }  // namespace
 
 struct lb_graph {
     int device = 0;
     int64_t S = 0, A = 0, E = 0;
     int32_t start = 0, max_ilabel = 0;
+    int64_t A_emit = 0;     // emitting arcs
+    int64_t max_edeg = 0;   // max emitting out-degree of a state
     int sms = 148;
     int4 *arcs = nullptr;
     unsigned *src = nullptr, *ol = nullptr, *off = nullptr, *eoff = nullptr;
@@ -128,40 +140,36 @@ struct lb_result {
     float t_decode = 0, t_prune = 0, t_h2d = 0, t_d2h = 0;
     int launches = 0;
     double phase_ms[8] = {0};   // lane-summed phase times (LB_PHASE_PROFILE=1 only)
+    double warp_ms[8] = {0};    // warp busy time per phase, summed over warps
+    double warp_n[8] = {0};     // warp-phase samples
 };
 
 namespace {
 
-int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, int path_cap, int tmax,
-                     bool packs, bool lat) {
+int ensure_workspace(lb_graph *g, int lanes, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap, int path_cap,
+                     int tmax, bool packs, bool lat) {
     Workspace &w = g->ws;
-    if (w.lanes >= lanes && w.S == g->S && w.tok_cap >= tok_cap && w.lat_cap >= lat_cap &&
-        w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat))
+    if (w.lanes >= lanes && w.C == C && w.S == g->S && w.ccap >= ccap && w.tok_cap >= tok_cap &&
+        w.lat_cap >= lat_cap && w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat))
         return LB_OK;
-    lanes = std::max(lanes, w.lanes);
-    tok_cap = std::max(tok_cap, w.tok_cap);
-    lat_cap = std::max(lat_cap, w.lat_cap);
-    path_cap = std::max(path_cap, w.path_cap);
-    tmax = std::max(tmax, w.tmax);
-    packs = packs || w.packs;
-    lat = lat || w.lat;
+    // Reallocate to exactly this request (never the max of old and new: the
+    // lane budget in decode_impl was computed for this request alone).
     w.release();
-    const size_t S = (size_t)g->S, nl = (size_t)lanes;
+    ccap = std::max<int64_t>(ccap, 1);
+    const size_t S = (size_t)g->S, nl = (size_t)lanes, nc = (size_t)C;
     auto A = [&](auto **p, size_t n) -> cudaError_t {
         cudaError_t e = dalloc(p, n);
         if (e == cudaSuccess) w.owned.push_back((void *)*p);
         return e;
     };
     CK(A(&w.rec, S * nl));
-    if (lat) CK(A(&w.minsnap, S * nl));
-    CK(A(&w.fc0, S * nl));
-    CK(A(&w.fc1, S * nl));
+    CK(A(&w.rpk, 2 * S * nl));
     CK(A(&w.tag, S * nl));
-    CK(A(&w.touched, S * nl));
-    CK(A(&w.fs0, S * nl));
-    CK(A(&w.fs1, S * nl));
-    CK(A(&w.fe0, S * nl));
-    CK(A(&w.fe1, S * nl));
+    CK(A(&w.touched, nc * S * nl));
+    CK(A(&w.fr, 2 * nc * S * nl));
+    CK(A(&w.fix, nc * S * nl));
+    CK(A(&w.cand, nc * (size_t)ccap * nl));
+    CK(A(&w.candi, nc * (size_t)ccap * nl));
     CK(A(&w.round_ctr, nl));
     const size_t tc = (size_t)tok_cap, lc = (size_t)std::max<int64_t>(lat_cap, 1);
     CK(A(&w.tok_state, tc * nl));
@@ -186,32 +194,33 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
     CK(A(&w.out_c, 8 * nl));
     CK(A(&w.d_lanes, nl));
     CK(A(&w.d_desc, nl));
-    CK(cudaMemsetAsync(w.rec, 0xFF, S * nl * sizeof(StateRec), g->stream));
+    init_rec<<<g->sms * 4, 256, 0, g->stream>>>(w.rec, (long long)(S * nl));
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(w.rpk, 0xFF, 2 * S * nl * sizeof(EpsWin), g->stream));
     CK(cudaMemsetAsync(w.tag, 0, S * nl * 4, g->stream));
     CK(cudaMemsetAsync(w.round_ctr, 0, nl * 4, g->stream));
-    if (lat) {
-        fill_f64<<<g->sms * 4, 256, 0, g->stream>>>(w.minsnap, INFINITY, (long long)(S * nl));
-        CK(cudaGetLastError());
-    }
     std::vector<LaneWs> hl(nl);
     for (size_t l = 0; l < nl; l++) {
         LaneWs &x = hl[l];
         x.rec = w.rec + l * S;
-        x.minsnap = lat ? w.minsnap + l * S : nullptr;
+        x.rpk = w.rpk + l * 2 * S;
         x.tag = w.tag + l * S;
-        x.touched = w.touched + l * S;
-        x.fs0 = w.fs0 + l * S;
-        x.fs1 = w.fs1 + l * S;
-        x.fc0 = w.fc0 + l * S;
-        x.fc1 = w.fc1 + l * S;
-        x.fe0 = w.fe0 + l * S;
-        x.fe1 = w.fe1 + l * S;
+        x.touched = w.touched + l * nc * S;
+        x.fr = w.fr + l * 2 * nc * S;
+        x.fix = w.fix + l * nc * S;
+        x.cand = w.cand + l * nc * (size_t)ccap;
+        x.candi = w.candi + l * nc * (size_t)ccap;
+        x.ccap = ccap;
         x.round_ctr = w.round_ctr + l;
+        x.S = (int)S;
+        x.C = C;
     }
     CK(cudaMemcpyAsync(w.d_lanes, hl.data(), nl * sizeof(LaneWs), cudaMemcpyHostToDevice, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     w.lanes = lanes;
+    w.C = C;
     w.S = g->S;
+    w.ccap = ccap;
     w.tok_cap = tok_cap;
     w.lat_cap = lat ? lat_cap : 0;
     w.path_cap = path_cap;
@@ -219,6 +228,17 @@ int ensure_workspace(lb_graph *g, int lanes, int64_t tok_cap, int64_t lat_cap, i
     w.packs = packs;
     w.lat = lat;
     return LB_OK;
+}
+
+// Candidate capacity per CTA: a frame's emitting candidates come from the previous
+// frame's tokens (<= max_tok, enforced per frame); warps stride over groups of 32
+// tokens, so a CTA of nw warps expands at most nw * ceil(groups / gnw) * 32 tokens.
+int64_t cand_capacity(const lb_graph *g, int64_t max_tok, int C, int threads) {
+    const int64_t groups = (max_tok + 31) / 32;
+    const int64_t nw = threads / 32, gnw = nw * C;
+    const int64_t tok_cta = nw * ((groups + gnw - 1) / gnw) * 32;
+    // + one partly used chunk per warp (sentinel tails, Lane::emit)
+    return std::min<int64_t>(g->A_emit, tok_cta * g->max_edeg) + nw * CAND_CHUNK + CAND_CHUNK;
 }
 
 UttDesc slot_desc(const Workspace &w, int l, const double *costs, int T, int64_t tok_cap = -1,
@@ -304,6 +324,10 @@ void fill_message(UttHost &u, int code, int frame, double aux, const lb_config &
             u.status = LB_INTERNAL;
             snprintf(buf, sizeof buf, "backtrace exceeded its step bound (epsilon cycle at frame %d)", frame);
             break;
+        case E_CAP_CAND:
+            u.status = LB_INTERNAL;
+            snprintf(buf, sizeof buf, "emitting candidate buffer overflowed at frame %d (sized by construction)", frame);
+            break;
         case E_INT_PRUNE_EPS:
             u.status = LB_INTERNAL;
             snprintf(buf, sizeof buf, "epsilon extra-cost fixpoint did not settle within frame %d", frame);
@@ -323,9 +347,9 @@ int validate_cfg(const lb_config *c) {
     if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
     if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
     if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
-    if (c->threads_per_lane != 0 && c->threads_per_lane != 256 && c->threads_per_lane != 512 &&
-        c->threads_per_lane != 768 && c->threads_per_lane != 1024)
-        return set_err(LB_USAGE, "threads_per_lane must be 256, 512, 768 or 1024");
+    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 640 &&
+        c->threads_per_lane != 768)
+        return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
     if (c->ctas_per_lane < 0 || c->ctas_per_lane > 4) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 4]");
     return LB_OK;
 }
@@ -344,20 +368,22 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
-    // lanes: requested, else as many as fit a memory budget (<= 2 waves of SMs)
-    const size_t per_lane = (size_t)S * (80 + (lat ? 8 : 0)) + (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) +
-                            (size_t)lat_cap * 28 + (size_t)path_cap * 4 + (size_t)(tmax + 2) * 16 + 256;
+    const int C = cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2;
+    const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
+    const int64_t ccap = cand_capacity(g, max_tok, C, threads);
+    // lanes: requested, else as many as fit a memory budget (<= 1 wave of SMs)
+    const size_t per_lane = lane_bytes(S, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t reuse = (size_t)g->ws.lanes * per_lane;
+    const size_t reuse = g->ws.C == C ? (size_t)g->ws.lanes *
+        lane_bytes(S, C, g->ws.ccap, g->ws.tok_cap, g->ws.lat_cap, g->ws.path_cap, g->ws.tmax, g->ws.packs, g->ws.lat) : 0;
     const size_t budget = (size_t)((double)(free_b + reuse) * 0.85);
-    const int C = cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2;
     int lanes = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / C));
     lanes = std::max(1, std::min(lanes, n > 0 ? n : 1));
     while (lanes > 1 && (size_t)lanes * per_lane > budget) lanes--;
     if ((size_t)lanes * per_lane > budget)
         return set_err(LB_CAPACITY, "not enough device memory for one decode lane; lower token_arena / max_lattice_arcs");
-    int rc = ensure_workspace(g, lanes, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    int rc = ensure_workspace(g, lanes, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
     if (rc) return rc;
     Workspace &w = g->ws;
 
@@ -371,16 +397,18 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     p.want_lattice = lat;
     p.collect_packs = packs;
     const size_t acrow_bytes = (size_t)D * 8;
-    p.acrow_smem = acrow_bytes <= 160 * 1024;
+    p.acrow_smem = acrow_bytes <= 120 * 1024;
     p.prof = nullptr;
+    const char *ex = getenv("LB_EXP");
+    p.exp = ex ? atoi(ex) : 0;
     const char *pe = getenv("LB_PHASE_PROFILE");
     unsigned long long *d_prof = nullptr;
     if (pe && pe[0] == '1') {
-        CK(cudaMalloc((void **)&d_prof, 8 * sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st));
+        CK(cudaMalloc((void **)&d_prof, 24 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(d_prof, 0, 24 * sizeof(unsigned long long), st));
         p.prof = d_prof;
     }
-    const size_t smem = p.acrow_smem ? acrow_bytes : 0;
+    const size_t smem = lane_dyn_smem(threads, D, p.acrow_smem != 0);
     // decode-lane variants: CTA size x batch width x lattice x phase-profile
     using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, int);
     const bool prof = p.prof != nullptr;
@@ -388,10 +416,10 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     (lat ? (prof ? decode_kernel<NT, U, true, true> : decode_kernel<NT, U, true, false>) \
          : (prof ? decode_kernel<NT, U, false, true> : decode_kernel<NT, U, false, false>))
     KernT kern;
-    if (threads == 1024) kern = LB_PICK(1024, 2);
-    else if (threads == 768) kern = LB_PICK(768, 2);
+    if (threads == 768) kern = LB_PICK(768, 2);
+    else if (threads == 640) kern = LB_PICK(640, 4);
     else if (threads == 512) kern = LB_PICK(512, 4);
-    else return set_err(LB_USAGE, "threads_per_lane must be 512, 768 or 1024");
+    else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
 #undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();
@@ -507,9 +535,13 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     cudaEventDestroy(e2);
     cudaEventDestroy(e3);
     if (d_prof) {
-        unsigned long long h[8];
+        unsigned long long h[24];
         CK(cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost));
-        for (int k = 0; k < 8; k++) res->phase_ms[k] = h[k] / 1e6;
+        for (int k = 0; k < 8; k++) {
+            res->phase_ms[k] = h[k] / 1e6;
+            res->warp_ms[k] = h[8 + k] / 1e6;
+            res->warp_n[k] = (double)h[16 + k];
+        }
         cudaFree(d_prof);
     }
     return LB_OK;
@@ -587,6 +619,16 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     }
     g->max_ilabel = maxil;
     g->E = (int64_t)heps.size();
+    // emitting-arc statistics (candidate buffer bound) and the "dst owns epsilon
+    // arcs" flag in bit 31 of the ilabel word (lb_device.cuh EPS_FLAG)
+    for (int64_t s = 0; s < S; s++) {
+        int64_t d = 0;
+        for (int64_t a = off[s]; a < off[s + 1]; a++) d += il[a] != 0;
+        g->A_emit += d;
+        g->max_edeg = std::max(g->max_edeg, d);
+    }
+    for (int64_t a = 0; a < A; a++)
+        if (heoff[dst[a] + 1] > heoff[dst[a]]) arcs[a].y = (int)((unsigned)arcs[a].y | EPS_FLAG);
     CK(dalloc(&g->arcs, A));
     CK(dalloc(&g->src, A));
     CK(dalloc(&g->ol, A));
@@ -799,6 +841,13 @@ int lb_result_phases(const lb_result *r, double *ms8) {
     return LB_OK;
 }
 
+int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8) {
+    if (!r || !busy_ms8 || !samples8) return set_err(LB_USAGE, "NULL argument");
+    std::memcpy(busy_ms8, r->warp_ms, sizeof(r->warp_ms));
+    std::memcpy(samples8, r->warp_n, sizeof(r->warp_n));
+    return LB_OK;
+}
+
 void lb_result_free(lb_result *r) { delete r; }
 
 static int expand_common(lb_graph *g, const int32_t *states, const double *costs, int64_t n, const double *acrow,
@@ -807,7 +856,8 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     if (!g || !states || !costs || n < 1) return set_err(LB_USAGE, "frontier is empty");
     std::lock_guard<std::mutex> lock(g->mu);
     CK(cudaSetDevice(g->device));
-    int rc = ensure_workspace(g, 1, n + g->S, 0, 16, 1, false, false);
+    const int64_t ccap = std::min<int64_t>(g->A_emit, n * g->max_edeg) + 25 * CAND_CHUNK;
+    int rc = ensure_workspace(g, 1, 1, ccap, n + g->S, 0, 16, 1, false, false);
     if (rc) return rc;
     Workspace &w = g->ws;
     cudaStream_t st = g->stream;
@@ -824,7 +874,6 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     LaneWs L;
     CK(cudaMemcpyAsync(&L, w.d_lanes, sizeof(LaneWs), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (mode == 0) setup_tokens<<<(int)((n + 255) / 256), 256, 0, st>>>(L.rec, d.tok_state, d.tok_cost, (int)n);
     Params p;
     std::memset(&p, 0, sizeof(p));
     p.beam = beam;
@@ -832,8 +881,10 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     p.max_tokens = 1ll << 40;
     p.D = D;
     p.acrow_smem = 0;
-    CK(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8));
-    expand_kernel<<<1, 1024, 8, st>>>(g->dev(), p, L, d, (int)n, mode, cutoff);
+    p.exp = 0;
+    const int esm = (int)lane_dyn_smem(768, 1, false);
+    CK(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, esm));
+    expand_kernel<<<1, 768, esm, st>>>(g->dev(), p, L, d, (int)n, mode, cutoff);
     CK(cudaGetLastError());
     int oi[8];
     double od[4];

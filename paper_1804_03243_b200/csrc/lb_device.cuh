@@ -32,11 +32,16 @@ enum : int {
     E_INT_INIT = 9,          // InternalInvariantError: initial token found at frame f
     E_INT_BACKTRACE = 10,    // InternalInvariantError: backtrace exceeded its step bound
     E_INT_PRUNE_EPS = 11,    // InternalInvariantError: eps extra-cost fixpoint
+    E_CAP_CAND = 12,         // CapacityError: candidate buffer (sized by construction; never expected)
 };
 
 // Graph replica in HBM.  Arc record = 16 B {dst, ilabel, weight};
-// epsilon arcs additionally get a per-state CSR of 16 B {dst, arc id, weight}
-// records so the closure reads one record per epsilon arc.
+// bit 31 of the ilabel word flags "dst owns epsilon out-arcs" (ilabels are
+// int32 >= 0, so the bit is free) so the emitting pass knows, for free, which
+// winners must enter the epsilon closure.  Epsilon arcs additionally get a
+// per-state CSR of 16 B {dst, arc id, weight} records so the closure reads one
+// record per epsilon arc.
+constexpr unsigned EPS_FLAG = 0x80000000u;
 struct GraphDev {
     const int4 *arcs;
     const unsigned *src;
@@ -53,26 +58,66 @@ struct GraphDev {
     int _pad;
 };
 
+__device__ __forceinline__ unsigned arc_il(int y) { return (unsigned)y & ~EPS_FLAG; }
+
 // Per-state record of a lane: everything a touched state needs in ONE 32-byte
-// sector.  cost[] is double-buffered by frame parity so the previous frame's
-// token cost of a source state stays readable while the current frame writes.
+// sector, laid out so each phase touches it with as few scattered accesses as
+// possible (the decode is bound by scattered L2 accesses per SM):
+//   [0,16)  cost, pred, tokidx  -- a winner writes all three in ONE 16 B store
+//   [16,24) pack                -- the 64-bit (cost, arc) word, SENT = untouched
+//   [24,32) minsnap             -- min epsilon-source snapshot (lattice rule A.5)
+// `pred` = (prev token index << 1) | 1 for an emitting winner, source state << 1
+// for an epsilon winner; `tokidx` = index in the newest frame's token list.
 struct __align__(32) StateRec {
-    unsigned long long pack;   // packed (cost, arc) word, SENT = untouched
-    double cost[2];            // f64 winner cost of frame t in cost[t & 1]
-    int pred;                  // (prev token index << 1) | 1  or  (source state << 1)
-    int tokidx;                // token index in the newest frame (sparse-set check)
+    double cost;
+    int pred;
+    int tokidx;
+    unsigned long long pack;
+    double minsnap;
 };
 
-// Per-lane scratch, all indexed by state (O(S) once, reset O(touched) per frame).
+// A winner's {cost, pred, tokidx = -1} in one 16-byte store (the stale token
+// index of an older frame is dead once the frame's emit barrier has passed).
+__device__ __forceinline__ void store_winner(StateRec *r, double cost, int pred) {
+    const unsigned long long hi = (unsigned long long)(unsigned)pred | 0xFFFFFFFF00000000ull;
+    asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(r),
+                 "l"((unsigned long long)__double_as_longlong(cost)), "l"(hi)
+                 : "memory");
+}
+// The whole record in one 32-byte store.
+__device__ __forceinline__ void store_rec32(StateRec *r, double cost, int pred, int tokidx,
+                                            unsigned long long pack, double minsnap) {
+    const unsigned long long x1 = (unsigned long long)(unsigned)pred | ((unsigned long long)(unsigned)tokidx << 32);
+    asm volatile("st.global.cg.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(r),
+                 "l"((unsigned long long)__double_as_longlong(cost)), "l"(x1), "l"(pack),
+                 "l"((unsigned long long)__double_as_longlong(minsnap))
+                 : "memory");
+}
+
+// Round-local epsilon winner of a state: the min improving offer's word and the
+// f64 cost of that same offer, updated together by a 128-bit CAS.  Idle value:
+// all ones (word SENT).
+struct __align__(16) EpsWin {
+    unsigned long long word;
+    unsigned long long cost_bits;
+};
+
+// Per-lane scratch.  O(S) arrays are allocated once and reset
+// O(touched) per frame.  Lists marked [C] have one S-sized segment per CTA of
+// the lane (CTA-local append counters in shared memory, no DSMEM traffic).
 struct LaneWs {
-    StateRec *rec;
-    double *minsnap;        // min frontier snapshot cost this frame (lattice eps rule)
-    unsigned *tag;          // epsilon round tag
-    unsigned *touched;
-    unsigned *fs0, *fs1;    // epsilon frontier: state,
-    double *fc0, *fc1;      //   snapshot cost,
-    uint2 *fe0, *fe1;       //   epsilon record range
-    unsigned *round_ctr;    // persistent per-lane round counter
+    StateRec *rec;             // [S]
+    EpsWin *rpk;               // [2][S] epsilon round winners by round parity
+    unsigned *tag;             // [S] epsilon round tag
+    unsigned *touched;         // [C][S] states touched this frame
+    unsigned *fr;              // [2][C][S] epsilon frontier by round parity
+    unsigned *fix;             // [C][S] tokens whose predecessor is an epsilon source state
+    int4 *cand;                // [C][ccap] emitting candidates {dst|flag, arc, cost_lo, cost_hi}
+    int *candi;                // [C][ccap] source token index of each candidate
+    long long ccap;            // candidate capacity per CTA
+    unsigned *round_ctr;       // persistent per-lane round counter
+    int S;
+    int C;
 };
 
 // One utterance slot of a wave.
@@ -108,6 +153,7 @@ struct Params {
     int collect_packs;
     int acrow_smem;
     unsigned long long *prof;   // optional per-phase ns accumulators (LB_PHASE_PROFILE=1)
+    int exp;                    // timing experiments (LB_EXP, profiling only; results not exact)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -130,52 +176,64 @@ __device__ __forceinline__ double dec64(unsigned long long e) {
     unsigned long long u = (e >> 63) ? (e ^ 0x8000000000000000ull) : ~e;
     return __longlong_as_double((long long)u);
 }
+// One 32-byte request for a whole state record (sm_100 256-bit LDG, L2 only).
 struct RecView {
-    unsigned long long pack;
-    double cost0, cost1;
+    double cost;
     int pred, tokidx;
-    __device__ __forceinline__ double cost(int parity) const { return parity ? cost1 : cost0; }
+    unsigned long long pack;
+    double minsnap;
 };
-
-__device__ __forceinline__ RecView load_rec(const StateRec *r) {
-    const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2 *>(r));
-    const ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2 *>(r) + 1);
-    RecView v;
-    v.pack = a.x;
-    v.cost0 = __longlong_as_double((long long)a.y);
-    v.cost1 = __longlong_as_double((long long)b.x);
-    v.pred = (int)(unsigned)(b.y & 0xFFFFFFFFull);
-    v.tokidx = (int)(unsigned)(b.y >> 32);
-    return v;
-}
-
-// One 32-byte request for a whole state record (sm_100 256-bit LDG/STG, L2 only).
 __device__ __forceinline__ RecView load_rec32(const StateRec *r) {
     unsigned long long x0, x1, x2, x3;
     asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
-                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(r) : "memory");
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(r));
     RecView v;
-    v.pack = x0;
-    v.cost0 = __longlong_as_double((long long)x1);
-    v.cost1 = __longlong_as_double((long long)x2);
-    v.pred = (int)(unsigned)(x3 & 0xFFFFFFFFull);
-    v.tokidx = (int)(unsigned)(x3 >> 32);
+    v.cost = __longlong_as_double((long long)x0);
+    v.pred = (int)(unsigned)(x1 & 0xFFFFFFFFull);
+    v.tokidx = (int)(unsigned)(x1 >> 32);
+    v.pack = x2;
+    v.minsnap = __longlong_as_double((long long)x3);
     return v;
 }
-__device__ __forceinline__ void store_rec32(StateRec *r, unsigned long long pack, double c0, double c1,
-                                            int pred, int tokidx) {
-    const unsigned long long x3 = (unsigned long long)(unsigned)pred | ((unsigned long long)(unsigned)tokidx << 32);
-    asm volatile("st.global.cg.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(r), "l"(pack),
-                 "l"((unsigned long long)__double_as_longlong(c0)), "l"((unsigned long long)__double_as_longlong(c1)),
-                 "l"(x3)
-                 : "memory");
+
+// 128-bit compare-and-swap (sm_90+): returns the previous value.
+__device__ __forceinline__ ulonglong2 cas128(EpsWin *p, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, v, d;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.relaxed.gpu.global.cas.b128 d, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+        : "memory");
+    return old;
+}
+
+// Keep the smaller (word, cost) pair: CAS loop from the idle value.  Words of one
+// round are unique (each epsilon arc is offered at most once per round).
+__device__ __forceinline__ void epswin_min(EpsWin *p, unsigned long long word, double cost) {
+    ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
+    const ulonglong2 val = make_ulonglong2(word, (unsigned long long)__double_as_longlong(cost));
+    for (;;) {
+        const ulonglong2 prev = cas128(p, cur, val);
+        if (prev.x == cur.x && prev.y == cur.y) return;
+        if (prev.x <= word) return;
+        cur = prev;
+    }
+}
+
+// Fire-and-forget 64-bit min at L2 (REDG): the issuing thread never waits.
+__device__ __forceinline__ void red_min_u64(unsigned long long *a, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void load_arc(const int4 *arcs, unsigned a, unsigned &dst, unsigned &il,
                                          double &w) {
     int4 r = __ldg(arcs + a);
     dst = (unsigned)r.x;
-    il = (unsigned)r.y;
+    il = arc_il(r.y);
     w = __hiloint2double(r.w, r.z);
 }
 
@@ -190,6 +248,33 @@ __device__ __forceinline__ int agg_append(int *counter) {
     base = __shfl_sync(mask, base, leader);
     return base + rank;
 }
+
+// Warp-staged list append (warp-collective: all 32 lanes call push/flush
+// together).  Items collect in a per-warp shared-memory stage and reach the
+// global list in bulk: ONE counter atomic per flush instead of one per warp
+// batch, so the warps of a CTA never serialize on a shared counter.
+constexpr int SW = 128;
+struct WStage {
+    unsigned *buf;   // SW entries of this warp's stage
+    int n;           // staged count (warp-uniform)
+    __device__ __forceinline__ void flush(int *counter, unsigned *out) {
+        __syncwarp();
+        if (n == 0) return;
+        int base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, n);
+        base = __shfl_sync(FULL, base, 0);
+        for (int i = threadIdx.x & 31; i < n; i += 32) __stcg(out + base + i, buf[i]);
+        __syncwarp();
+        n = 0;
+    }
+    __device__ __forceinline__ void push(bool pred, unsigned val, int *counter, unsigned *out) {
+        const int lane = threadIdx.x & 31;
+        const unsigned m = __ballot_sync(FULL, pred);
+        if (pred) buf[n + __popc(m & ((1u << lane) - 1u))] = val;
+        n += __popc(m);
+        if (n > SW - 32) flush(counter, out);
+    }
+};
 
 __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll

@@ -4,32 +4,35 @@
 // utterance of a wave (the paper's sequence parallelism, as
 // lanes instead of MPS processes).  The lane walks the utterance's frames in
 // order; inside a frame its C CTAs split every phase below and meet at cluster
-// barriers.  The lane's counters (touched / frontier / token / lattice list
-// lengths, error flag) live in the shared memory of the cluster's rank-0 CTA and
-// are updated through distributed shared memory, so no frame ever leaves the
-// GPU.  Fewer, wider lanes keep every lane's hot per-state records L2-resident
-// (SURVEY.md §7 step 7).  Hot loops are batched UNR-wide so every thread keeps
-// UNR independent gathers / atomics in flight.
+// barriers.  Lane-wide counters (token / lattice list lengths, error flag) live
+// in the rank-0 CTA's shared memory and are reached through DSMEM; every other
+// list (candidates, touched states, epsilon frontiers, fixes) is CTA-local with
+// a shared-memory append counter, so the hot loops never wait on a remote
+// atomic.  No frame ever leaves the GPU.
 //
 //   emit      warp-cooperative expansion of the previous frame's tokens: the warp
 //             takes 32 tokens, prefix-scans their out-degrees with shuffles
 //             (Alg. 2 / static partition, scheduler.py:60-78) and walks the
 //             flattened arc range 32*UNR arcs at a time, each lane binary-
-//             searching its owner token with shuffles; 16 B arc loads; one 64-bit
-//             atomicMin per candidate on the packed (cost, arc) word (Alg. 1,
-//             decoder.py:189-205); states seen for the first time (old ==
-//             sentinel) go to the touched list (one DSMEM atomic per warp).  The
-//             frame best is a cluster min over ALL candidates.
-//   winners   per touched state: the winner's f64 cost is recomputed from its
-//             arc and its source token's cost (same operands, same order =>
-//             bit-identical to the offer); seed if cost <= cutoff; max-active
-//             histogram (per CTA, merged through DSMEM).
-//   epsilon   Jacobi rounds (reference.py:160-192): phase A offers pack words
-//             from snapshot costs, phase B lets the round's unique winning offer
-//             write the state's f64 cost / source.
+//             searching its owner token with shuffles; 16 B arc loads; one
+//             fire-and-forget 64-bit RED.MIN per candidate on the packed
+//             (cost, arc) word (Alg. 1, decoder.py:189-205) and a coalesced
+//             append of the candidate {dst, arc, cost, token} to the CTA's
+//             candidate buffer.  The frame best is a cluster min over ALL
+//             candidates (decoder.py:533-539).
+//   winners   per candidate: it owns its state iff the state's final word is its
+//             own word (arc ids make words unique); the owner records the
+//             state's f64 cost / predecessor (decoder.py:314-327), lists the state
+//             as touched, seeds the epsilon frontier and the max-active histogram.
+//   epsilon   Jacobi rounds (reference.py:160-192) with ONE cluster barrier per
+//             round: a frontier state first recovers its cost from the previous
+//             round's round-local winning word (rpk, a second 64-bit min that only
+//             improving offers reach) and its source's parked snapshot, then
+//             offers from that snapshot.  Round barriers keep the reference's
+//             snapshot semantics bit-exact.
 //   aggregate touched states under the cutoff become the frame's token list
 //             (device order; the host sorts by state when lists are read back);
-//             the same pass resets the state's pack word (O(touched), not O(S)).
+//             the same pass resets the state word (O(touched), not O(S)).
 //   lattice   live arcs by rule A.5: emitting arc live iff its
 //             candidate <= cutoff and its destination was kept; epsilon arc live
 //             iff both ends kept and min-snapshot(src) + w <= cutoff.
@@ -42,19 +45,20 @@ namespace lbk {
 
 namespace cgx = cooperative_groups;
 
-// Shared state of a lane.  Lane-wide fields are authoritative in the rank-0 CTA
-// (reached through DSMEM); they are double-buffered by frame parity (and the
-// epsilon frontier length by round parity) so a frame needs no barrier just to
-// reset counters: the set for frame t+1 is cleared while frame t runs.
+// Shared state of a lane CTA.  Lane-wide fields are authoritative in the rank-0
+// CTA; per-CTA fields are this CTA's append counters.  Counters are
+// double-buffered by frame parity (epsilon frontier lengths by round mod 3) so
+// the set for frame t+1 is cleared while frame t runs, without a barrier.
 struct Smem {
-    int ntouched[2], ntok[2], nfix[2], nlat[2];
-    int nfr[3];                    // epsilon frontier lengths (round mod 3)
-    int nseed[2];                  // seeds (winners <= cutoff) per frame parity
-    unsigned long long best[2];    // order-preserving f64 frame best (frame parity)
+    // lane-wide (rank 0)
+    int ntok[2], nlat[2];
     int err, err_frame;
     long long err_aux;
-    unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
     // per CTA
+    int ntouched[2], ncand[2], nseed[2], nfix[2];
+    int nfr[3];
+    unsigned long long best[2];    // order-preserving f64 running best (frame parity)
+    unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
     unsigned round_id;             // epsilon round tag (identical in every CTA of the lane)
     double red0;
     int ired0;
@@ -115,18 +119,40 @@ __device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
 
 // Warp-cooperative load-balanced walk over every (token, out-arc) pair of a
 // token list, UNR arcs per lane per batch; warps of all CTAs of the lane share
-// the list.  f(valid[], i[], arc[], cost[]) receives one batch.
+// the list.  Per group of 32 tokens the warp prefix-scans the out-degrees with
+// shuffles (the static partition of scheduler.py:60-78 at warp granularity);
+// each token then writes its lane id over its arc slots in a per-warp shared
+// memory map (`own`, WMAP slots), so an arc slot finds its owner token with ONE
+// shared load instead of a 5-step shuffle binary search (the search remains as
+// the fallback for groups wider than the map).  The next group's tokens are
+// fetched while the current group's arcs are walked.  f(valid[], i[], arc[],
+// cost[]) receives one batch; the batch loop is warp-uniform, so f may use
+// full-mask warp collectives.
+constexpr int WMAP = 512;
 template <int UNR, class F>
 __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, const Grp &G,
                                                            const unsigned *ts, const double *tc, int n,
-                                                           unsigned &c_scan, F &&f) {
+                                                           unsigned &c_scan, int *own, F &&f) {
     const int lane = threadIdx.x & 31;
-    for (int base = G.gwarp() * 32; base < n; base += G.gnw() * 32) {
-        const int i = base + lane;
-        const bool valid = i < n;
-        const unsigned s = valid ? __ldcg(ts + i) : 0u;
-        const double c = valid ? __ldcg(tc + i) : 0.0;
+    const int step = G.gnw() * 32;
+    int base = G.gwarp() * 32;
+    unsigned s = 0u;
+    double c = 0.0;
+    if (base + lane < n) {
+        s = __ldcg(ts + base + lane);
+        c = __ldcg(tc + base + lane);
+    }
+    for (; base < n; base += step) {
+        const bool valid = base + lane < n;
         const uint2 rg = valid ? __ldg(g.rng + s) : make_uint2(0u, 0u);
+        // prefetch the next group's tokens
+        const int nb = base + step;
+        unsigned s_n = 0u;
+        double c_n = 0.0;
+        if (nb + lane < n) {
+            s_n = __ldcg(ts + nb + lane);
+            c_n = __ldcg(tc + nb + lane);
+        }
         const unsigned lo = rg.x;
         const int deg = (int)(rg.y - rg.x);
         int incl = deg;
@@ -138,6 +164,11 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
         const int excl = incl - deg;
         const int total = __shfl_sync(FULL, incl, 31);
         if (lane == 0) c_scan += (unsigned)total;
+        const bool mapped = total <= WMAP;
+        if (mapped) {
+            for (int j = excl; j < incl; j++) own[j] = lane;
+            __syncwarp();
+        }
         for (int j0 = 0; j0 < total; j0 += 32 * UNR) {
             bool vv[UNR];
             int ii[UNR];
@@ -147,10 +178,14 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
             for (int u = 0; u < UNR; u++) {
                 const int j = j0 + u * 32 + lane;
                 int k = 0;
+                if (mapped) {
+                    k = j < total ? own[j] : 0;
+                } else {
 #pragma unroll
-                for (int b = 16; b > 0; b >>= 1) {
-                    int t = __shfl_sync(FULL, incl, k + b - 1);
-                    if (t <= j) k += b;
+                    for (int b = 16; b > 0; b >>= 1) {
+                        int t = __shfl_sync(FULL, incl, k + b - 1);
+                        if (t <= j) k += b;
+                    }
                 }
                 const int ek = __shfl_sync(FULL, excl, k);
                 const unsigned lk = __shfl_sync(FULL, lo, k);
@@ -161,28 +196,83 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
             }
             f(vv, ii, aa, cc);
         }
+        if (mapped) __syncwarp();
+        s = s_n;
+        c = c_n;
     }
 }
 
-// Per-lane decode phases.  UNR = independent items per thread per batch.
+// Dynamic shared memory of a lane CTA of `threads` threads (see Lane::Lane).
+// Per-warp phase scratch (bytes), aliased between phases: winners uses two u32
+// stages of SW entries; aggregate a token stage of SWT entries {cost, minsnap,
+// state, arc, key, pred} and a u32 fix stage.
+constexpr int SWT = 64;
+constexpr int WSCR = SWT * 32 + SW * 4;
+static_assert(2 * SW * 4 <= WSCR, "winners stages fit the warp scratch");
+inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem) {
+    const size_t nw = (size_t)threads / 32;
+    return (acrow_smem ? (size_t)D * 8 : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
+}
+constexpr int CAND_CHUNK = 256;   // Lane::CCH
+
+// Per-lane decode phases.  UNR = independent arcs per thread per emit batch.
 template <int UNR>
 struct Lane {
+    static constexpr int WUNR = 4;   // candidates per thread per winners batch
+    static constexpr int AUNR = 2;   // touched states per thread per aggregate batch
+    static constexpr int EUNR = 2;   // frontier entries per thread per epsilon batch
     const GraphDev &g;      // __grid_constant__ kernel parameters: referenced in place,
     const Params &p;        // never copied to local memory
     const LaneWs &L;
     const UttDesc &io;
     const Grp G;
     double *acrow;          // shared-memory row (when p.acrow_smem)
+    int *own_base;          // per-warp arc-slot owner maps (WMAP ints per warp, shared memory)
+    char *scratch_base;     // per-warp phase scratch (WSCR bytes per warp, shared memory)
+    int *whist_base;        // per-warp max-active histograms (NBINS ints per warp, shared memory)
+    unsigned long long *wprof = nullptr;   // per-warp busy-time accumulators (profiling only)
     const double *row;      // global row of the current frame
-    int par;                // parity of the current frame (cost slot, counter set)
+    int par;                // parity of the current frame (counter set)
 
+    // Dynamic shared memory: [acrow: D f64 when p.acrow_smem][owner maps][stages][histograms]
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
-                    const Grp &G_, double *acrow_)
-        : g(g_), p(p_), L(L_), io(io_), G(G_), acrow(acrow_), row(nullptr), par(0) {}
+                    const Grp &G_, double *dyn)
+        : g(g_), p(p_), L(L_), io(io_), G(G_), acrow(dyn), row(nullptr), par(0) {
+        const int nw = blockDim.x >> 5;
+        own_base = reinterpret_cast<int *>(dyn + (p.acrow_smem ? p.D : 0));
+        scratch_base = reinterpret_cast<char *>(own_base + nw * WMAP);
+        whist_base = reinterpret_cast<int *>(scratch_base + nw * WSCR);
+    }
+    __device__ __forceinline__ char *scratch() const { return scratch_base + (threadIdx.x >> 5) * WSCR; }
+    // u32 stage q (0, 1) of this warp's scratch (winners)
+    __device__ __forceinline__ WStage stage(int q) const {
+        WStage st;
+        st.buf = reinterpret_cast<unsigned *>(scratch()) + q * SW;
+        st.n = 0;
+        return st;
+    }
 
-    __device__ __forceinline__ unsigned *fsb(int r) const { return (r & 1) ? L.fs1 : L.fs0; }
-    __device__ __forceinline__ double *fcb(int r) const { return (r & 1) ? L.fc1 : L.fc0; }
-    __device__ __forceinline__ uint2 *feb(int r) const { return (r & 1) ? L.fe1 : L.fe0; }
+    // Profiling aid: a warp's busy time inside a phase (up to its arrival at the
+    // phase's closing barrier), summed over warps; [ph] = ns, [8 + ph] = samples.
+    __device__ __forceinline__ unsigned long long wbegin() const { return wprof ? gtimer() : 0ull; }
+    __device__ __forceinline__ void wend(int ph, unsigned long long t0) const {
+        if (wprof) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                atomicAdd(wprof + ph, gtimer() - t0);
+                atomicAdd(wprof + 8 + ph, 1ull);
+            }
+        }
+    }
+
+    // this CTA's segments of the per-CTA lists
+    __device__ __forceinline__ unsigned *touched() const { return L.touched + (size_t)G.rank * L.S; }
+    __device__ __forceinline__ unsigned *front(int r) const {
+        return L.fr + ((size_t)(r & 1) * L.C + G.rank) * L.S;
+    }
+    __device__ __forceinline__ EpsWin *rpk(int r) const { return L.rpk + (size_t)(r & 1) * L.S; }
+    __device__ __forceinline__ unsigned *fixes() const { return L.fix + (size_t)G.rank * L.S; }
+    __device__ __forceinline__ int *wmap() const { return own_base + (threadIdx.x >> 5) * WMAP; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
         return p.acrow_smem ? acrow[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
@@ -201,94 +291,127 @@ struct Lane {
             for (int d = threadIdx.x; d < p.D; d += blockDim.x) acrow[d] = __dmul_rn(__ldg(r + d), p.scale);
     }
 
-    // Clear the counter set of the NEXT frame (leader only; its last readers are done).
+    // Clear the counter set of the NEXT frame (its previous readers are done).
     __device__ __forceinline__ void clear_next_counters() const {
-        if (G.leader()) {
-            Smem *M = G.M;
-            const int q = par ^ 1;
-            M->ntouched[q] = M->ntok[q] = M->nfix[q] = M->nlat[q] = M->nseed[q] = 0;
+        const int q = par ^ 1;
+        if (G.leader()) G.M->ntok[q] = G.M->nlat[q] = 0;
+        if (threadIdx.x == 0) {
+            G.S->ntouched[q] = G.S->ncand[q] = G.S->nseed[q] = G.S->nfix[q] = 0;
+            G.S->best[q] = SENT;
         }
-        if (threadIdx.x == 0) G.S->best[par ^ 1] = SENT;   // per-CTA partial of the next frame
-        for (int b = threadIdx.x; b < NBINS; b += blockDim.x) G.S->hist[par ^ 1][b] = 0;
     }
 
     // ---- emit: returns the lane-wide best candidate (one cluster barrier) ----
     // Every candidate feeds the frame best, but a candidate whose float32 key is
     // above the float32 key of a running upper bound of this frame's cutoff
-    // (running best + beam_eff) skips its atomic: it can neither be the best nor
-    // the winner of a state that survives the cutoff, and no epsilon offer (cost
+    // (running best + beam_eff) is dropped: it can neither be the best nor the
+    // winner of a state that survives the cutoff, and no epsilon offer (cost
     // <= cutoff) can tie with it, so every kept state's winner is unchanged.
-    __device__ double emit(const unsigned *pts, const double *ptc, int np, double beam_eff) {
-        double lbest = inf_d();
+    // The running best is one shared word per CTA, read every batch and pushed
+    // (one warp-aggregated atomic) only by a batch that improves it.  Surviving
+    // candidates go to the CTA's candidate buffer in per-warp chunks of CCH
+    // slots (one counter atomic per chunk); a chunk's unused tail is filled
+    // with sentinels (x = -1) that winners() skips.
+    static constexpr int CCH = CAND_CHUNK;
+    __device__ double emit(const unsigned *pts, const double *ptc, int np, double beam_eff, int frame) {
         StateRec *rec = L.rec;
         unsigned c_scan = 0, c_cand = 0;
-        int *ntouched = &G.M->ntouched[par];
+        int *ncand = &G.S->ncand[par];
+        int4 *cb = L.cand + (size_t)G.rank * L.ccap;
+        int *cbi = L.candi + (size_t)G.rank * L.ccap;
+        const long long ccap = L.ccap;
         unsigned long long *run = &G.S->best[par];
-        unsigned bound_key = 0xFFFFFFFFu;     // enc32 of the running cutoff bound
-        if (G.leader()) G.M->nfr[0] = G.M->nfr[1] = G.M->nfr[2] = 0;
-        for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan,
-                                        [&](const bool *vv, const int *, const unsigned *aa, const double *cc) {
+        const int lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1u;
+        int cstart = 0, cused = CCH;          // current chunk (warp-uniform); none yet
+        bool overflow = false;
+        if (threadIdx.x == 0) G.S->nfr[0] = G.S->nfr[1] = G.S->nfr[2] = 0;
+        const unsigned long long t0 = wbegin();
+        auto fill_tail = [&]() {
+            for (int i = cused + lane; i < CCH; i += 32) __stcg(cb + cstart + i, make_int4(-1, 0, 0, 0));
+        };
+        for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan, wmap(),
+                                        [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
             int4 r[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++)
                 if (vv[u]) r[u] = __ldg(g.arcs + aa[u]);
+            unsigned long long known = *(volatile unsigned long long *)run;
             double cand[UNR];
             double bmin = inf_d();
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 cand[u] = inf_d();
-                if (vv[u] && r[u].y != 0) {
+                const unsigned il = vv[u] ? arc_il(r[u].y) : 0u;
+                if (il != 0) {
                     const double w = __hiloint2double(r[u].w, r[u].z);
-                    cand[u] = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r[u].y));
+                    cand[u] = __dadd_rn(__dadd_rn(cc[u], w), ac(il));
                     bmin = fmin(bmin, cand[u]);
                 }
             }
-            lbest = fmin(lbest, bmin);
-            // share the running best through the CTA (one shared atomic per warp batch)
-            bmin = warp_min(bmin);
-            unsigned long long rb = 0;
-            if ((threadIdx.x & 31) == 0) {
-                const unsigned long long e = enc64(bmin);
-                const unsigned long long o = atomicMin(run, e);
-                rb = o < e ? o : e;
+            unsigned long long eb = enc64(bmin);
+            if (__any_sync(FULL, eb < known)) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(FULL, eb, o);
+                    eb = x < eb ? x : eb;
+                }
+                if (lane == 0) atomicMin(run, eb);
+                known = eb < known ? eb : known;
             }
-            rb = __shfl_sync(FULL, rb, 0);
-            const double rbest = dec64(rb);
-            if (rbest < inf_d()) {
-                const unsigned k = (unsigned)(pack_word(__dadd_rn(rbest, beam_eff), 0u) >> 32);
-                bound_key = k < bound_key ? k : bound_key;
-            }
-            unsigned long long old[UNR];
+            unsigned bound_key = 0xFFFFFFFFu;     // enc32 of the running cutoff bound
+            if (known != SENT) bound_key = (unsigned)(pack_word(__dadd_rn(dec64(known), beam_eff), 0u) >> 32);
             bool em[UNR];
+            int off[UNR];
+            int tot = 0;
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
-                em[u] = cand[u] < inf_d();
-                if (em[u]) {
+                em[u] = false;
+                if (cand[u] < inf_d()) {
                     const unsigned long long word = pack_word(cand[u], aa[u]);
                     em[u] = (unsigned)(word >> 32) <= bound_key;
+                    if (em[u]) red_min_u64(&rec[r[u].x].pack, word);
+                }
+                const unsigned bb = __ballot_sync(FULL, em[u]);
+                off[u] = tot + __popc(bb & lt);
+                tot += __popc(bb);
+            }
+            if (tot == 0) return;
+            c_cand += (lane == 0) ? (unsigned)tot : 0u;
+            if (cused + tot > CCH) {
+                if (cused < CCH) fill_tail();
+                int nb = 0;
+                if (lane == 0) nb = atomicAdd(ncand, CCH);
+                cstart = __shfl_sync(FULL, nb, 0);
+                cused = 0;
+                if ((long long)cstart + CCH > ccap) {
+                    overflow = true;
+                    if (lane == 0) set_error(E_CAP_CAND, frame, (long long)cstart + CCH);
+                }
+            }
+            if (!overflow) {
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
                     if (em[u]) {
-                        old[u] = atomicMin(&rec[r[u].x].pack, word);
-                        c_cand++;
+                        const long long bits = __double_as_longlong(cand[u]);
+                        const unsigned flag = (unsigned)r[u].y & EPS_FLAG;
+                        const int k = cstart + cused + off[u];
+                        __stcg(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
+                                                 (int)(bits & 0xFFFFFFFFll), (int)(bits >> 32)));
+                        __stcg(cbi + k, ii[u]);
                     }
                 }
             }
-#pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (em[u] && old[u] == SENT) {
-                    const int sl = agg_append(ntouched);
-                    __stcg(L.touched + sl, (unsigned)r[u].x);
-                }
-            }
+            cused += tot;
         });
-        lbest = warp_min(lbest);
+        if (cused < CCH && !overflow) fill_tail();
         c_cand = warp_sum(c_cand);
         c_scan = warp_sum(c_scan);
-        if ((threadIdx.x & 31) == 0) {
-            // CTA-local shared atomics; the lane-wide min is merged after the barrier
-            atomicMin(run, enc64(lbest));
+        if (lane == 0) {
             atomicAdd(&G.S->c_cand, (unsigned long long)c_cand);
             atomicAdd(&G.S->c_scan, (unsigned long long)c_scan);
         }
+        wend(0, t0);
         G.sync();
         unsigned long long b = SENT;
         for (int q = 0; q < G.C; q++) {
@@ -298,75 +421,112 @@ struct Lane {
         return dec64(b);
     }
 
-    // ---- winners: f64 cost of every touched state; seeds; epsilon frontier (round 0); histogram ----
+    // Epsilon predecessors of the PREVIOUS frame's tokens (source state -> token
+    // index), run inside the next frame's emit phase so it needs no barrier of its
+    // own: the indices it reads were final at the previous aggregate barrier and
+    // are not rewritten before this frame's aggregate.  `fpar` = previous frame's
+    // parity (its fix count), `tbf`/`nf` = its token list.
+    __device__ void fix_preds(int fpar, int frame, long long tbf, int nf) {
+        const int mine = G.S->nfix[fpar];
+        const unsigned *fx = fixes();
+        for (int q = threadIdx.x; q < mine; q += blockDim.x) {
+            const long long o = tbf + (long long)__ldcg(fx + q);
+            const int u = __ldcg(io.tok_pred + o) >> 1;
+            const int pi = __ldcg(&L.rec[u].tokidx);
+            if (pi < 0 || pi >= nf || __ldcg(io.tok_state + tbf + pi) != (unsigned)u)
+                set_error(E_INT_EPS_PRED, frame, u);
+            __stcg(io.tok_pred + o, pi << 1);
+        }
+    }
+
+    // ---- winners: owners of the state words; seeds; epsilon frontier (round 0); histogram ----
+    // Warp-uniform loop over the CTA's candidate buffer (32*WUNR entries per warp
+    // step).  Appends go through per-warp shared-memory stages; the max-active
+    // histogram is per warp (match_any groups equal bins, the group leader does a
+    // plain read-modify-write) and is summed into the CTA histogram at the end,
+    // so no shared-memory atomic is ever contended.
     __device__ void winners(double cutoff, double best) {
-        const int nt = G.M->ntouched[par];
+        const int nc = G.S->ncand[par];
         const bool hist = p.max_active > 0;
-        const bool eps = g.has_eps;
         const double width = __ddiv_rn(p.beam, (double)NBINS);
-        const int pp = par ^ 1;
+        const int4 *cb = L.cand + (size_t)G.rank * L.ccap;
+        const int *cbi = L.candi + (size_t)G.rank * L.ccap;
         StateRec *rec = L.rec;
-        int *nfront = &G.M->nfr[0], *nseed = &G.M->nseed[par];
-        int *hst = G.S->hist[par];
-        const int stride = G.gstride();
-        for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
-            unsigned v[UNR];
-            bool ok[UNR];
+        unsigned *tl = touched();
+        unsigned *f0 = front(0);
+        int *ntouched = &G.S->ntouched[par], *nf0 = &G.S->nfr[0];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        int *wh = whist_base + warp * NBINS;
+        if (hist)
+            for (int b = lane; b < NBINS; b += 32) wh[b] = 0;
+        __syncwarp();
+        WStage st_t = stage(0), st_f = stage(1);
+        unsigned nseed = 0;
+        const unsigned long long t0 = wbegin();
+        for (int kb = warp * 32 * WUNR; kb < nc; kb += nw * 32 * WUNR) {
+            int4 e[WUNR];
+            int ti[WUNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                const int k = k0 + u * stride;
-                ok[u] = k < nt;
-                v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
-            }
-            unsigned a[UNR];
-            uint2 er[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                a[u] = ok[u] ? (unsigned)__ldcg(&rec[v[u]].pack) : 0u;
-                er[u] = (ok[u] && eps) ? __ldg(g.erng + v[u]) : make_uint2(0u, 0u);
-            }
-            int4 ar[UNR];
-            unsigned src[UNR];
-#pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (ok[u]) {
-                    ar[u] = __ldg(g.arcs + a[u]);
-                    src[u] = __ldg(g.src + a[u]);
+            for (int u = 0; u < WUNR; u++) {
+                const int k = kb + u * 32 + lane;
+                e[u].x = -1;
+                if (k < nc) {
+                    e[u] = __ldcg(cb + k);
+                    if (e[u].x != -1) ti[u] = __ldcg(cbi + k);
                 }
             }
-            double pc[UNR];
-            int pi[UNR];
+            unsigned long long pk[WUNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (ok[u]) {
-                    const RecView sr = load_rec32(&rec[src[u]]);
-                    pc[u] = sr.cost(pp);
-                    pi[u] = sr.tokidx;
-                }
-            }
+            for (int u = 0; u < WUNR; u++)
+                pk[u] = e[u].x != -1 ? __ldcg(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (!ok[u]) continue;
-                const double w = __hiloint2double(ar[u].w, ar[u].z);
-                const double cand = __dadd_rn(__dadd_rn(pc[u], w), ac((unsigned)ar[u].y));
-                __stcg(&rec[v[u]].cost[par], cand);
-                __stcg(&rec[v[u]].pred, (pi[u] << 1) | 1);
-                if (cand <= cutoff) {
-                    agg_append(nseed);
-                    if (er[u].x < er[u].y) {      // only states with epsilon arcs enter the closure
-                        const int sl = agg_append(nfront);
-                        __stcg(L.fs0 + sl, v[u]);
-                        __stcg(L.fc0 + sl, cand);
-                        __stcg(L.fe0 + sl, er[u]);
+            for (int u = 0; u < WUNR; u++) {
+                const unsigned v = (unsigned)e[u].x & ~EPS_FLAG;
+                const double cand = __hiloint2double(e[u].w, e[u].z);
+                const bool own = e[u].x != -1 && pk[u] == pack_word(cand, (unsigned)e[u].y);
+                if (own) store_winner(&rec[v], cand, (ti[u] << 1) | 1);
+                st_t.push(own, v, ntouched, tl);
+                const bool seed = own && cand <= cutoff;
+                nseed += seed;
+                // only states with epsilon arcs enter the closure
+                st_f.push(seed && ((unsigned)e[u].x & EPS_FLAG), v, nf0, f0);
+                if (hist) {
+                    int bin = NBINS + lane;       // unique dummy key for non-seeds
+                    if (seed) {
+                        const double q = (p.exp & 1) ? __dmul_rn(__dsub_rn(cand, best), 1.0 / width)
+                                                     : __ddiv_rn(__dsub_rn(cand, best), width);
+                        bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
                     }
-                    if (hist) {
-                        const double q = __ddiv_rn(__dsub_rn(cand, best), width);
-                        const int bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
-                        atomicAdd(&hst[bin], 1);
+                    if (p.exp & 2) {
+                        if (seed) atomicAdd(wh + bin, 1);
+                    } else {
+                        const unsigned grp = __match_any_sync(FULL, bin);
+                        if (seed && lane == __ffs(grp) - 1) wh[bin] += __popc(grp);
+                        __syncwarp();
                     }
                 }
             }
         }
+        st_t.flush(ntouched, tl);
+        st_f.flush(nf0, f0);
+        nseed = warp_sum(nseed);
+        if (lane == 0 && nseed) atomicAdd(&G.S->nseed[par], (int)nseed);
+        wend(1, t0);
+        if (hist) {
+            __syncthreads();
+            for (int b = threadIdx.x; b < NBINS; b += blockDim.x) {
+                int sum = 0;
+                for (int w = 0; w < nw; w++) sum += whist_base[w * NBINS + b];
+                G.S->hist[par][b] = sum;
+            }
+        }
+    }
+
+    // Lane-wide seed count (after the barrier that follows winners()).
+    __device__ __forceinline__ int lane_seeds() const {
+        int s = 0;
+        for (int q = 0; q < G.C; q++) s += G.at(q)->nseed[par];
+        return s;
     }
 
     // max-active cutoff: H = best + max(b*,1)*width, b* = first
@@ -418,113 +578,97 @@ struct Lane {
         return r;
     }
 
-    // Keep the round-0 epsilon frontier entries with cost <= cutoff (after a
-    // max-active tightening): buffer 0 -> buffer 1 (count nfr[1]), one batched
-    // pass and one barrier; the epsilon closure then starts at round 1.
-    __device__ void filter_seeds(double cutoff) {
-        const int nf = G.M->nfr[0];
-        int *nout = &G.M->nfr[1];
-        const int stride = G.gstride();
-        for (int k0 = G.gtid(); k0 < nf; k0 += 4 * stride) {
-            double c[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int k = k0 + u * stride;
-                c[u] = k < nf ? __ldcg(L.fc0 + k) : inf_d();
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                if (c[u] <= cutoff) {
-                    const int k = k0 + u * stride;
-                    const int sl = agg_append(nout);
-                    __stcg(L.fs1 + sl, __ldcg(L.fs0 + k));
-                    __stcg(L.fc1 + sl, c[u]);
-                    __stcg(L.fe1 + sl, __ldcg(L.fe0 + k));
-                }
-            }
-        }
-        G.sync();
-    }
-
-    // ---- epsilon closure under a fixed cutoff: Jacobi rounds, two barriers each ----
-    // Round r reads frontier buffer (r&1) = (state, snapshot cost, epsilon range),
-    // count nfr[r%3].  Phase A: each entry parks its snapshot in its record's
-    // cost[par^1] slot (dead after winners), offers pack words, and tags improved
-    // states (the first tagger appends the state to the next frontier).  Phase B:
-    // for each improved state the winning arc is read from the pack; its f64 cost
-    // is recomputed from the source's parked snapshot (same operands => the
-    // winning offer's exact value) and written with the source as predecessor.
-    __device__ bool epsilon(double cutoff, int frame, int r0 = 0) {
+    // ---- epsilon closure under a fixed cutoff: Jacobi rounds, ONE barrier each ----
+    // Round r processes this CTA's frontier F_r (states improved in round r-1;
+    // round 0 = seeds).  Every improving offer of round r-1 to v also entered the
+    // pair (word, f64 cost) into rpk[(r-1)&1][v] with a 128-bit CAS-min, so the
+    // round winner's word AND its exact f64 cost are one 16-byte load away
+    // (offers of round r go to the other buffer and cannot disturb it).  v
+    // adopts that cost, then offers from it: exactly the reference's snapshot
+    // semantics (reference.py:160-192).
+    __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
         StateRec *rec = L.rec;
-        const int stride = G.gstride();
-        const int pp = par ^ 1;
         unsigned round_id = G.S->round_id;
         unsigned c_escan = 0, c_ecand = 0, c_front = 0;
+        unsigned *tl = touched();
+        int *ntouched = &G.S->ntouched[par];
+        const int bd = blockDim.x;
         bool ok = true;
-        for (int r = r0;; r++) {
-            const int nf = G.M->nfr[r % 3];
-            if (nf == 0) break;
+        for (int r = 0;; r++) {
+            int total = 0;
+            for (int q = 0; q < G.C; q++) total += G.at(q)->nfr[r % 3];
+            if (total == 0) break;
             if (r > g.S + 1) {
                 if (G.leader()) set_error(E_INT_EPS_ROUNDS, frame, 0);
                 ok = false;
                 break;
             }
             ++round_id;
-            const unsigned *fs = fsb(r);
-            const double *fc = fcb(r);
-            const uint2 *fe = feb(r);
-            unsigned *fsn = fsb(r + 1);
-            double *fcn = fcb(r + 1);
-            uint2 *fen = feb(r + 1);
-            int *nnext = &G.M->nfr[(r + 1) % 3];
-            if (G.leader()) G.M->nfr[(r + 2) % 3] = 0;   // read at round r-1's start, two barriers ago
-            // phase A: offers from snapshot costs
-            for (int k = G.gtid(); k < nf; k += stride) {
-                const double cu = __ldcg(fc + k);
-                if (!(cu <= cutoff)) continue;
-                const unsigned u = __ldcg(fs + k);
-                const uint2 er = __ldcg(fe + k);
-                c_front++;
-                if (LAT) {
-                    const double m = __ldcg(L.minsnap + u);
-                    if (cu < m) __stcg(L.minsnap + u, cu);
+            const int nf = G.S->nfr[r % 3];
+            const unsigned *fs = front(r);
+            unsigned *fsn = front(r + 1);
+            int *nnext = &G.S->nfr[(r + 1) % 3];
+            if (threadIdx.x == 0) G.S->nfr[(r + 2) % 3] = 0;   // read at round r-1's start, one barrier ago
+            EpsWin *rprev = rpk(r + 1);                         // == rpk(r - 1)
+            EpsWin *rcur = rpk(r);
+            const unsigned long long t0 = wbegin();
+            for (int k0 = threadIdx.x; k0 < nf; k0 += EUNR * bd) {
+                unsigned v[EUNR];
+                uint2 er[EUNR];
+                double c[EUNR];
+#pragma unroll
+                for (int u = 0; u < EUNR; u++) {
+                    const int k = k0 + u * bd;
+                    v[u] = k < nf ? __ldcg(fs + k) : 0xFFFFFFFFu;
                 }
-                __stcg(&rec[u].cost[pp], cu);
-                c_escan += er.y - er.x;
-                for (unsigned e = er.x; e < er.y; ++e) {
-                    const int4 rr = __ldg(g.eps + e);
-                    const double cand = __dadd_rn(cu, __hiloint2double(rr.w, rr.z));
-                    if (!(cand <= cutoff)) continue;
-                    c_ecand++;
-                    const unsigned v = (unsigned)rr.x;
-                    const unsigned long long word = pack_word(cand, (unsigned)rr.y);
-                    const unsigned long long old = atomicMin(&rec[v].pack, word);
-                    if (old == SENT) {
-                        const int sl = agg_append(&G.M->ntouched[par]);
-                        __stcg(L.touched + sl, v);
+#pragma unroll
+                for (int u = 0; u < EUNR; u++) {
+                    if (v[u] == 0xFFFFFFFFu) continue;
+                    er[u] = __ldg(g.erng + v[u]);
+                    if (r == 0) {
+                        c[u] = __ldcg(&rec[v[u]].cost);
+                    } else {
+                        const ulonglong2 w2 = __ldcg(reinterpret_cast<const ulonglong2 *>(rprev + v[u]));
+                        __stcg(reinterpret_cast<ulonglong2 *>(rprev + v[u]), make_ulonglong2(~0ull, ~0ull));
+                        c[u] = __longlong_as_double((long long)w2.y);
+                        const unsigned src = __ldg(g.src + (unsigned)w2.x);
+                        store_winner(&rec[v[u]], c[u], (int)(src << 1));
                     }
-                    if (old > word && atomicExch(L.tag + v, round_id) != round_id) {
-                        const int sl = agg_append(nnext);
-                        __stcg(fsn + sl, v);
+                }
+#pragma unroll
+                for (int u = 0; u < EUNR; u++) {
+                    if (v[u] == 0xFFFFFFFFu) continue;
+                    if (!(c[u] <= cutoff)) continue;      // round-0 seeds above a max-active cutoff
+                    c_front++;
+                    if (LAT) {
+                        const double m = __ldcg(&rec[v[u]].minsnap);
+                        if (c[u] < m) __stcg(&rec[v[u]].minsnap, c[u]);
+                    }
+                    c_escan += er[u].y - er[u].x;
+                    for (unsigned e = er[u].x; e < er[u].y; ++e) {
+                        const int4 rr = __ldg(g.eps + e);
+                        const double cand = __dadd_rn(c[u], __hiloint2double(rr.w, rr.z));
+                        if (!(cand <= cutoff)) continue;
+                        c_ecand++;
+                        const unsigned x = (unsigned)rr.x;
+                        const unsigned long long word = pack_word(cand, (unsigned)rr.y);
+                        const unsigned long long old = atomicMin(&rec[x].pack, word);
+                        if (old == SENT) {
+                            const int sl = agg_append(ntouched);
+                            __stcg(tl + sl, x);
+                        }
+                        if (old > word) {
+                            epswin_min(rcur + x, word, cand);
+                            if (atomicExch(L.tag + x, round_id) != round_id) {
+                                const int sl = agg_append(nnext);
+                                __stcg(fsn + sl, x);
+                            }
+                        }
                     }
                 }
             }
-            G.sync();
-            // phase B: improved states recover their round winner from the pack
-            const int nn = *nnext;
-            for (int k = G.gtid(); k < nn; k += stride) {
-                const unsigned v = __ldcg(fsn + k);
-                const unsigned a = (unsigned)__ldcg(&rec[v].pack);
-                const double w = __ldg(reinterpret_cast<const double *>(g.arcs + a) + 1);
-                const unsigned u = __ldg(g.src + a);
-                const uint2 er = __ldg(g.erng + v);
-                const double cand = __dadd_rn(__ldcg(&rec[u].cost[pp]), w);
-                __stcg(&rec[v].cost[par], cand);
-                __stcg(&rec[v].pred, (int)(u << 1));
-                __stcg(fcn + k, cand);
-                __stcg(fen + k, er);
-            }
+            wend(3, t0);
             G.sync();
         }
         c_escan = warp_sum(c_escan);
@@ -541,52 +685,118 @@ struct Lane {
     }
 
     // ---- aggregate + reset: frame token list at io.tok_*[tb ...]; returns count or -1 ----
+    // Warp-uniform loop over this CTA's touched list: ONE 32-byte record load
+    // per touched state.  A dropped state's word is reset at once; a kept state
+    // is staged per warp with everything its token needs, and a stage flush
+    // takes lane-wide token indices in bulk (one DSMEM counter atomic per flush),
+    // writes the token records (coalesced) and the state record in ONE 32-byte
+    // store (token index set, word reset).  Tokens whose predecessor is an
+    // epsilon source STATE go to this CTA's fix list; fix_preds() maps them to
+    // token indices during the next frame's emit.
+    struct TokStage {
+        double *cost, *msnap;
+        unsigned *v, *arc, *key;
+        int *pred;
+        int n;
+    };
+    __device__ __forceinline__ TokStage tok_stage() const {
+        char *b = scratch();
+        TokStage t;
+        t.cost = reinterpret_cast<double *>(b);
+        t.msnap = t.cost + SWT;
+        t.v = reinterpret_cast<unsigned *>(t.msnap + SWT);
+        t.arc = t.v + SWT;
+        t.key = t.arc + SWT;
+        t.pred = reinterpret_cast<int *>(t.key + SWT);
+        t.n = 0;
+        return t;
+    }
+    __device__ __forceinline__ WStage fix_stage() const {
+        WStage st;
+        st.buf = reinterpret_cast<unsigned *>(scratch() + SWT * 32);
+        st.n = 0;
+        return st;
+    }
+
+    __device__ void flush_tokens(TokStage &st, WStage &sf, int frame, long long tb, long long room) {
+        __syncwarp();
+        if (st.n == 0) return;
+        const int lane = threadIdx.x & 31;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&G.M->ntok[par], st.n);
+        base = __shfl_sync(FULL, base, 0);
+        StateRec *rec = L.rec;
+        for (int i0 = 0; i0 < st.n; i0 += 32) {
+            const int i = i0 + lane;
+            bool fx = false;
+            const int idx = base + i;
+            if (i < st.n && idx < room) {
+                const unsigned v = st.v[i];
+                const bool init = frame == 0 && (int)v == g.start;
+                const double c = st.cost[i];
+                const int pr = st.pred[i];
+                const long long o = tb + idx;
+                __stcg(io.tok_state + o, v);
+                __stcg(io.tok_cost + o, init ? 0.0 : c);
+                __stcg(io.tok_arc + o, init ? -1 : (int)st.arc[i]);
+                __stcg(io.tok_pred + o, init ? -1 : pr);
+                if (p.collect_packs)
+                    __stcg(io.tok_pack + o, ((unsigned long long)st.key[i] << 32) | st.arc[i]);
+                store_rec32(&rec[v], c, pr, idx, SENT, st.msnap[i]);
+                fx = !init && (pr & 1) == 0;
+            } else if (i < st.n) {
+                __stcg(&rec[st.v[i]].pack, SENT);   // over the arena: error raised after the barrier
+            }
+            sf.push(fx, (unsigned)idx, &G.S->nfix[par], fixes());
+        }
+        __syncwarp();
+        st.n = 0;
+    }
+
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = G.M->ntouched[par];
+        const int nt = G.S->ntouched[par];
         const long long room = io.tok_cap - tb;
         StateRec *rec = L.rec;
-        unsigned *fix = L.fs1;  // scratch: tokens whose predecessor is an epsilon source state
-        int *ntok = &G.M->ntok[par], *nfix = &G.M->nfix[par];
-        const int stride = G.gstride();
-        for (int k0 = G.gtid(); k0 < nt; k0 += UNR * stride) {
-            unsigned v[UNR];
-            bool ok[UNR];
+        const unsigned *tl = touched();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        const unsigned lt = (1u << lane) - 1u;
+        TokStage st = tok_stage();
+        WStage sf = fix_stage();
+        const unsigned long long t0 = wbegin();
+        for (int kb = warp * 32 * AUNR; kb < nt; kb += nw * 32 * AUNR) {
+            unsigned v[AUNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                const int k = k0 + u * stride;
-                ok[u] = k < nt;
-                v[u] = ok[u] ? __ldcg(L.touched + k) : 0u;
+            for (int u = 0; u < AUNR; u++) {
+                const int k = kb + u * 32 + lane;
+                v[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
             }
-            RecView r[UNR];
+            RecView rv[AUNR];
 #pragma unroll
-            for (int u = 0; u < UNR; u++)
-                if (ok[u]) r[u] = load_rec32(&rec[v[u]]);
+            for (int u = 0; u < AUNR; u++)
+                if (v[u] != 0xFFFFFFFFu) rv[u] = load_rec32(&rec[v[u]]);
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
-                if (!ok[u]) continue;
-                const bool init = frame == 0 && (int)v[u] == g.start;
-                const double c = init ? 0.0 : r[u].cost(par);
-                int tidx = r[u].tokidx;
-                if (init || c <= cutoff) {
-                    const int idx = agg_append(ntok);
-                    if (idx < room) {
-                        const long long o = tb + idx;
-                        __stcg(io.tok_state + o, v[u]);
-                        __stcg(io.tok_cost + o, c);
-                        __stcg(io.tok_arc + o, init ? -1 : (int)(unsigned)r[u].pack);
-                        __stcg(io.tok_pred + o, init ? -1 : r[u].pred);
-                        if (p.collect_packs) __stcg(io.tok_pack + o, r[u].pack);
-                        tidx = idx;
-                        if (!init && (r[u].pred & 1) == 0) {
-                            const int f = agg_append(nfix);
-                            __stcg(fix + f, (unsigned)idx);
-                        }
-                    }
+            for (int u = 0; u < AUNR; u++) {
+                const bool valid = v[u] != 0xFFFFFFFFu;
+                const bool init = valid && frame == 0 && (int)v[u] == g.start;
+                const bool keep = valid && (init || rv[u].cost <= cutoff);
+                if (valid && !keep) __stcg(&rec[v[u]].pack, SENT);
+                const unsigned m = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int j = st.n + __popc(m & lt);
+                    st.v[j] = v[u];
+                    st.cost[j] = rv[u].cost;
+                    st.msnap[j] = rv[u].minsnap;
+                    st.arc[j] = (unsigned)rv[u].pack;
+                    st.key[j] = (unsigned)(rv[u].pack >> 32);
+                    st.pred[j] = rv[u].pred;
                 }
-                __stcg(&rec[v[u]].pack, SENT);
-                if (tidx != r[u].tokidx) __stcg(&rec[v[u]].tokidx, tidx);
+                st.n += __popc(m);
+                if (st.n > SWT - 32) flush_tokens(st, sf, frame, tb, room);
             }
         }
+        flush_tokens(st, sf, frame, tb, room);
+        sf.flush(&G.S->nfix[par], fixes());
+        wend(4, t0);
         G.sync();
         const int n = G.M->ntok[par];
         if (n == 0 || (long long)n > p.max_tokens || (long long)n > room) {
@@ -597,20 +807,6 @@ struct Lane {
             }
             G.sync();
             return -1;
-        }
-        // epsilon predecessors: source state -> token index of this frame
-        const int nfx = G.M->nfix[par];
-        if (nfx > 0) {
-            for (int q = G.gtid(); q < nfx; q += stride) {
-                const long long o = tb + (long long)__ldcg(fix + q);
-                const int u = __ldcg(io.tok_pred + o) >> 1;
-                const int pi = __ldcg(&rec[u].tokidx);
-                if (pi < 0 || pi >= n || __ldcg(io.tok_state + tb + pi) != (unsigned)u)
-                    set_error(E_INT_EPS_PRED, frame, u);
-                __stcg(io.tok_pred + o, pi << 1);
-            }
-            G.sync();
-            if (G.M->err) return -1;
         }
         return n;
     }
@@ -635,15 +831,16 @@ struct Lane {
                            long long lb) {
         if (frame > 0) {
             unsigned dummy = 0;
-            for_each_token_arc_batched<UNR>(g, G, io.tok_state + tbp, io.tok_cost + tbp, np, dummy,
+            for_each_token_arc_batched<UNR>(g, G, io.tok_state + tbp, io.tok_cost + tbp, np, dummy, wmap(),
                                             [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
 #pragma unroll
                 for (int u = 0; u < UNR; u++) {
                     if (!vv[u]) continue;
                     const int4 r = __ldg(g.arcs + aa[u]);
-                    if (r.y == 0) continue;
+                    const unsigned il = arc_il(r.y);
+                    if (il == 0) continue;
                     const double w = __hiloint2double(r.w, r.z);
-                    const double cand = __dadd_rn(__dadd_rn(cc[u], w), ac((unsigned)r.y));
+                    const double cand = __dadd_rn(__dadd_rn(cc[u], w), ac(il));
                     int j;
                     if (cand <= cutoff && kept((unsigned)r.x, tb, n, j)) lat_push((int)aa[u], ii[u], j, lb);
                 }
@@ -654,8 +851,8 @@ struct Lane {
             for (int j = G.gtid(); j < n; j += G.gstride()) {
                 const unsigned u = __ldcg(io.tok_state + tb + j);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                const double ms = __ldcg(L.minsnap + u);
-                __stcg(L.minsnap + u, inf);
+                const double ms = __ldcg(&L.rec[u].minsnap);
+                __stcg(&L.rec[u].minsnap, inf);
                 for (unsigned e = e0; e < e1; ++e) {
                     const int4 r = __ldg(g.eps + e);
                     int jv;
@@ -674,15 +871,18 @@ struct Lane {
         return nl;
     }
 
-    // ---- error path: O(touched) reset of every state word this frame touched ----
+    // ---- error path: O(touched) reset of every per-state word this frame touched ----
     __device__ void reset_touched() {
         G.sync();
-        const int nt = G.M->ntouched[par];
+        const int nt = G.S->ntouched[par];
+        const unsigned *tl = touched();
         const double inf = inf_d();
-        for (int k = G.gtid(); k < nt; k += G.gstride()) {
-            const unsigned v = __ldcg(L.touched + k);
+        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+            const unsigned v = __ldcg(tl + k);
             __stcg(&L.rec[v].pack, SENT);
-            if (p.want_lattice) __stcg(L.minsnap + v, inf);
+            __stcg(&L.rec[v].minsnap, inf);
+            __stcg(reinterpret_cast<ulonglong2 *>(rpk(0) + v), make_ulonglong2(~0ull, ~0ull));
+            __stcg(reinterpret_cast<ulonglong2 *>(rpk(1) + v), make_ulonglong2(~0ull, ~0ull));
         }
         G.sync();
     }
@@ -691,7 +891,8 @@ struct Lane {
 __device__ __forceinline__ void init_smem(Smem &sm, unsigned round_ctr) {
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; q++) {
-            sm.ntouched[q] = sm.ntok[q] = sm.nfix[q] = sm.nlat[q] = sm.nseed[q] = 0;
+            sm.ntok[q] = sm.nlat[q] = 0;
+            sm.ntouched[q] = sm.ncand[q] = sm.nseed[q] = sm.nfix[q] = 0;
             sm.best[q] = SENT;
         }
         sm.nfr[0] = sm.nfr[1] = sm.nfr[2] = 0;
@@ -700,12 +901,28 @@ __device__ __forceinline__ void init_smem(Smem &sm, unsigned round_ctr) {
         sm.round_id = round_ctr;
         sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
-    for (int b = threadIdx.x; b < 2 * NBINS; b += blockDim.x) sm.hist[b / NBINS][b % NBINS] = 0;
+}
+
+// Seed the start state (frame 0, decoder.py:510-513) into the rank-0 CTA's lists.
+template <int UNR>
+__device__ __forceinline__ void seed_start(Lane<UNR> &ln, const GraphDev &g, const LaneWs &L) {
+    if (ln.G.leader()) {
+        StateRec *r = &L.rec[g.start];
+        __stcg(&r->pack, pack_word(0.0, 0u));
+        __stcg(&r->cost, 0.0);
+        __stcg(&r->pred, -1);
+        __stcg(ln.touched(), (unsigned)g.start);
+        ln.G.S->ntouched[0] = 1;
+        if (g.has_eps) {
+            __stcg(ln.front(0), (unsigned)g.start);
+            ln.G.S->nfr[0] = 1;
+        }
+    }
 }
 
 // ===========================================================================
 // Full-utterance decode: one cluster (lane) per utterance of the wave.
-// Cluster barriers per frame: emit 1, winners 1, epsilon 2 per round,
+// Cluster barriers per frame: emit 1, winners 1, epsilon 1 per round,
 // aggregate 1-2, lattice 1.
 // ===========================================================================
 template <int NT, int UNR, bool LAT, bool PROF>
@@ -728,6 +945,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     G.sync();
 
     Lane<UNR> ln(g, p, L, io, G, s_acrow);
+    if (PROF) ln.wprof = p.prof + 8;
     const int T = io.T;
     const double inf = inf_d();
     long long tb = 0, lb = 0;
@@ -748,16 +966,8 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
 
     // ---- frame 0 (decoder.py:510-523): start token, epsilon closure ----
     ln.par = 0;
+    seed_start(ln, g, L);
     if (G.leader()) {
-        __stcg(&L.rec[g.start].pack, pack_word(0.0, 0u));
-        __stcg(&L.rec[g.start].cost[0], 0.0);
-        __stcg(&L.rec[g.start].pred, -1);
-        __stcg(L.touched, (unsigned)g.start);
-        __stcg(L.fs0, (unsigned)g.start);
-        __stcg(L.fc0, 0.0);
-        __stcg(L.fe0, g.has_eps ? __ldg(g.erng + g.start) : make_uint2(0u, 0u));
-        sm.ntouched[0] = 1;
-        sm.nfr[0] = 1;
         io.tok_base[0] = 0;
         if (LAT) io.lat_base[0] = 0;
     }
@@ -790,8 +1000,9 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         ln.par = t & 1;
         reset_done = false;
         ln.load_row(io.costs + (long long)(t - 1) * p.D);
+        if (g.has_eps) ln.fix_preds((t - 1) & 1, t - 1, tbp, np);
         __syncthreads();
-        const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff);
+        const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff, t);
         ln.clear_next_counters();   // frame t-1's readers are past the emit barrier
         mark(0);
         if (!(best < inf)) {
@@ -799,27 +1010,23 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
             ok = false;
             break;
         }
+        if (G.M->err) { ok = false; break; }   // candidate buffer overflow (never by construction)
         cutoff = __dadd_rn(best, beam_eff);
         ln.winners(cutoff, best);
         G.sync();
         mark(1);
-        const int nf = G.M->nseed[ln.par];
+        const int nf = ln.lane_seeds();
         if (nf == 0) {
             if (G.leader()) ln.set_error(E_DEAD_NO_TOKENS, t, 0);
             ok = false;
             break;
         }
-        int r0 = 0;
         bool tightened = false;
         if (p.max_active > 0 && nf > p.max_active) {
             const double c2 = ln.max_active_cutoff(cutoff, best);
             if (c2 < cutoff) {
                 tightened = true;
                 cutoff = c2;
-                if (g.has_eps) {   // without epsilon arcs the seeds are never read again
-                    ln.filter_seeds(cutoff);
-                    r0 = 1;
-                }
             }
         }
         // Kaldi's adaptive beam: after a max-active tightening the next frame's beam
@@ -832,7 +1039,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         }
         mark(2);
         if (g.has_eps) {
-            ok = ln.epsilon(cutoff, t, r0);
+            ok = ln.epsilon(cutoff, t);
             if (!ok) break;
         }
         mark(3);
@@ -855,6 +1062,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         tdone = t;
     }
     if (!ok && !reset_done) ln.reset_touched();
+    if (ok && g.has_eps) ln.fix_preds(T & 1, T, tb, ntok);   // the last frame's epsilon predecessors
     G.sync();
 
     // ---- counters: per-CTA partials merged through DSMEM ----
@@ -1015,7 +1223,7 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
                 __syncthreads();
                 for (long long k = k0 + tid; k < k1; k += bd) {
                     const unsigned a = (unsigned)__ldcg(io.lat_arc + k);
-                    if ((unsigned)__ldg(g.arcs + a).y != 0) continue;
+                    if (arc_il(__ldg(g.arcs + a).y) != 0) continue;
                     atomicMin(ne + __ldcg(io.lat_from + k), enc64(io.tmp[k]));
                 }
                 __syncthreads();
@@ -1055,13 +1263,12 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
 
 // ===========================================================================
 // Single-op surfaces (decoder.py:373-435), one CTA (a cluster of one).
-//   mode 0 = expand_emitting: tokens at io.tok_*[0..n), whose states carry
-//            (cost[0], tokidx) from setup_tokens; acrow (scaled) at io.costs;
-//            writes winners <= cutoff to io.tok_state/tok_cost[n ...].
+//   mode 0 = expand_emitting: tokens at io.tok_*[0..n); acrow (scaled) at
+//            io.costs; writes winners <= cutoff to io.tok_state/tok_cost[n ...].
 //   mode 1 = expand_nonemitting: seeds at io.tok_*[0..n) act as won entries
 //            pack(cost, 0); closes under `cutoff`; writes the merged frontier.
 // ===========================================================================
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(768, 1)
 expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
               const __grid_constant__ LaneWs L, const __grid_constant__ UttDesc io, int n, int mode,
               double cutoff_in) {
@@ -1081,7 +1288,7 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     if (mode == 0) {
         ln.load_row(io.costs);
         __syncthreads();
-        const double best = ln.emit(io.tok_state, io.tok_cost, n, p.beam);
+        const double best = ln.emit(io.tok_state, io.tok_cost, n, p.beam, 1);
         if (!(best < inf_d())) {
             cutoff = inf_d();
         } else {
@@ -1093,12 +1300,10 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
             const unsigned s = __ldcg(io.tok_state + i);
             const double c = __ldcg(io.tok_cost + i);
             __stcg(&L.rec[s].pack, pack_word(c, 0u));
-            __stcg(&L.rec[s].cost[1], c);
+            __stcg(&L.rec[s].cost, c);
             __stcg(&L.rec[s].pred, -1);
-            __stcg(L.touched + i, s);
-            __stcg(L.fs0 + i, s);
-            __stcg(L.fc0 + i, c);
-            __stcg(L.fe0 + i, g.has_eps ? __ldg(g.erng + s) : make_uint2(0u, 0u));
+            __stcg(ln.touched() + i, s);
+            __stcg(ln.front(0) + i, s);
         }
         __syncthreads();
         if (tid == 0) { sm.ntouched[1] = n; sm.nfr[0] = n; }
@@ -1109,9 +1314,10 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     }
     __syncthreads();
     const int nt = sm.ntouched[1];
+    const unsigned *tl = ln.touched();
     for (int k = tid; k < nt; k += blockDim.x) {
-        const unsigned v = __ldcg(L.touched + k);
-        const double c = __ldcg(&L.rec[v].cost[1]);
+        const unsigned v = __ldcg(tl + k);
+        const double c = __ldcg(&L.rec[v].cost);
         if (c <= cutoff) {
             const int idx = agg_append(&sm.ntok[1]);
             __stcg(io.tok_state + n + idx, v);
@@ -1123,20 +1329,21 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     if (tid == 0) {
         io.out_i[4] = sm.ntok[1];
         io.out_d[0] = cutoff;
+        if (sm.err && !io.out_i[0]) io.out_i[0] = sm.err;
         __stcg(L.round_ctr, sm.round_id);
     }
 }
 
-// Fill helpers.
-__global__ void fill_f64(double *p, double v, long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        p[i] = v;
-}
-// expand_emitting setup: the frontier's states carry (cost[0], tokidx) like a previous frame.
-__global__ void setup_tokens(StateRec *rec, const unsigned *states, const double *costs, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        rec[states[i]].cost[0] = costs[i];
-        rec[states[i]].tokidx = i;
+// Workspace initialisation: every state record idle (pack SENT, no token, minsnap +inf).
+__global__ void init_rec(StateRec *r, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        StateRec x;
+        x.pack = SENT;
+        x.cost = 0.0;
+        x.pred = -1;
+        x.tokidx = -1;
+        x.minsnap = inf_d();
+        r[i] = x;
     }
 }
 

@@ -83,8 +83,8 @@ class DecodeConfig:
                      "device"):
             if int(getattr(self, name)) < 0:
                 raise UsageError(f"{name} must be >= 0")
-        if int(self.threads_per_lane) not in (0, 256, 512, 768, 1024):
-            raise UsageError("threads_per_lane must be 256, 512, 768 or 1024")
+        if int(self.threads_per_lane) not in (0, 512, 640, 768):
+            raise UsageError("threads_per_lane must be 512, 640 or 768")
         if not 0 <= int(self.ctas_per_lane) <= 4:
             raise UsageError("ctas_per_lane must be in [0, 4]")
 

@@ -57,8 +57,13 @@ def decode_batch_resident(wfst, tensors, config: DecodeConfig | None = None, str
         tm = result_timing(res)
         ph = np.zeros(8)
         L.lb_result_phases(res, ptr(ph, PD))
-        tm["phases_ms"] = dict(zip(("emit", "winners", "max_active", "epsilon", "aggregate", "lattice",
-                                    "turnover", "frame0_final"), ph.tolist()))
+        names = ("emit", "winners", "max_active", "epsilon", "aggregate", "lattice", "turnover",
+                 "frame0_final")
+        tm["phases_ms"] = dict(zip(names, ph.tolist()))
+        wb, wn = np.zeros(8), np.zeros(8)
+        L.lb_result_warp_phases(res, ptr(wb, PD), ptr(wn, PD))
+        tm["warp_busy_ms"] = dict(zip(names, wb.tolist()))
+        tm["warp_samples"] = dict(zip(names, wn.tolist()))
         return out, tm
     finally:
         L.lb_result_free(res)

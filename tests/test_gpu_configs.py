@@ -30,6 +30,16 @@ pytestmark = pytest.mark.gpu
 _GRAPHS: dict = {}
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _release_graphs():
+    """Drop the full-size graphs (and their device replicas + lane workspaces,
+    tens of GB at C4) before the next test module runs."""
+    yield
+    import gc
+    _GRAPHS.clear()
+    gc.collect()
+
+
 def graph(name):
     key = "C2" if name in ("C2", "C3", "C4") else name
     if key not in _GRAPHS:
