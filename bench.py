@@ -272,13 +272,15 @@ def main(argv=None):
     clocks.start()
     dist.barrier()
     torch.cuda.synchronize()
-    total_ms, kern_ms, launches, alg_bytes, arcs = 0.0, 0.0, 0, 0, 0
+    total_ms, kern_ms, launches, alg_bytes, arcs, host_ms = 0.0, 0.0, 0, 0, 0, 0.0
     for k in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         outs, tm = step_resident(args.warmup + k)
+        host_ms += (time.perf_counter() - h0) * 1e3
         e1.record(stream)
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
@@ -331,6 +333,7 @@ def main(argv=None):
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "decode_kernel", "alg_bytes_per_launch": alg_bytes / max(args.steps, 1),
                 "kernel_ms_per_launch": kern_ms / max(args.steps, 1),
+                "step_host_ms": host_ms / max(args.steps, 1),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
 
     cpu = None

@@ -224,6 +224,19 @@ __device__ __forceinline__ void epswin_min(EpsWin *p, unsigned long long word, d
     }
 }
 
+// Global-space atomics with their results (explicit .global: a generic 64-bit
+// atomicMin would carry a shared-memory CAS fallback path).
+__device__ __forceinline__ unsigned long long atom_min_u64(unsigned long long *a, unsigned long long v) {
+    unsigned long long o;
+    asm volatile("atom.relaxed.gpu.global.min.u64 %0, [%1], %2;" : "=l"(o) : "l"(a), "l"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ unsigned atom_exch_u32(unsigned *a, unsigned v) {
+    unsigned o;
+    asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(a), "r"(v) : "memory");
+    return o;
+}
+
 // Fire-and-forget 64-bit min at L2 (REDG): the issuing thread never waits.
 __device__ __forceinline__ void red_min_u64(unsigned long long *a, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");

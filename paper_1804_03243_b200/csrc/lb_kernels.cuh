@@ -67,15 +67,20 @@ struct Smem {
     int hist[2][NBINS];            // max-active histogram (frame parity)
 };
 
+// The lane CTA's shared state and dynamic shared memory, declared at namespace
+// scope so every phase addresses them as shared::cta directly (a generic
+// pointer into a cluster's shared window costs an address conversion per use).
+__shared__ Smem lane_sm;
+extern __shared__ double lane_dyn[];
+
 __device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7FF0000000000000ll); }
 
 // The cluster that runs one lane.
 struct Grp {
-    Smem *S;        // this CTA's shared state
     Smem *M;        // rank-0 CTA's shared state (DSMEM)
     int rank, C;
     __device__ __forceinline__ void sync() const { cgx::this_cluster().sync(); }
-    __device__ __forceinline__ Smem *at(int q) const { return cgx::this_cluster().map_shared_rank(S, q); }
+    __device__ __forceinline__ Smem *at(int q) const { return cgx::this_cluster().map_shared_rank(&lane_sm, q); }
     __device__ __forceinline__ int gtid() const { return rank * blockDim.x + threadIdx.x; }
     __device__ __forceinline__ int gstride() const { return C * blockDim.x; }
     __device__ __forceinline__ int gwarp() const { return rank * (blockDim.x >> 5) + (threadIdx.x >> 5); }
@@ -92,18 +97,18 @@ __device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
         int os = __shfl_xor_sync(FULL, s, o);
         if (ov < v || (ov == v && os < s)) { v = ov; s = os; }
     }
-    if (lane == 0) { G.S->red[warp] = v; G.S->ired[warp] = s; }
+    if (lane == 0) { lane_sm.red[warp] = v; lane_sm.ired[warp] = s; }
     __syncthreads();
     if (warp == 0) {
-        double x = lane < nw ? G.S->red[lane] : inf_d();
-        int y = lane < nw ? G.S->ired[lane] : 0x7FFFFFFF;
+        double x = lane < nw ? lane_sm.red[lane] : inf_d();
+        int y = lane < nw ? lane_sm.ired[lane] : 0x7FFFFFFF;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             double ov = __shfl_xor_sync(FULL, x, o);
             int os = __shfl_xor_sync(FULL, y, o);
             if (ov < x || (ov == x && os < y)) { x = ov; y = os; }
         }
-        if (lane == 0) { G.S->red0 = x; G.S->ired0 = y; }
+        if (lane == 0) { lane_sm.red0 = x; lane_sm.ired0 = y; }
     }
     G.sync();
     v = inf_d();
@@ -207,6 +212,7 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, co
 // stages of SW entries; aggregate a token stage of SWT entries {cost, minsnap,
 // state, arc, key, pred} and a u32 fix stage.
 constexpr int SWT = 64;
+constexpr size_t ACROW_SMEM_MAX = 48 * 1024;   // acoustic rows up to 6144 pdfs live in shared memory
 constexpr int WSCR = SWT * 32 + SW * 4;
 static_assert(2 * SW * 4 <= WSCR, "winners stages fit the warp scratch");
 inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem) {
@@ -215,10 +221,24 @@ inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem) {
 }
 constexpr int CAND_CHUNK = 256;   // Lane::CCH
 
+// Max-active histogram bin of a seed:
+// min(NBINS-1, max(0, trunc(RN((c - best) / width)))) exactly.  The quotient is
+// taken as a product with the rounded reciprocal, and recomputed with a true
+// division only when that product lies within 1e-9 of an integer (the only
+// place the two can truncate differently), so the bin is bit-exact with the
+// oracle's division at a fraction of its cost.
+__device__ __forceinline__ int hist_bin(double c, double best, double width, double inv_w) {
+    const double d = __dsub_rn(c, best);
+    double q = __dmul_rn(d, inv_w);
+    const double fr = q - floor(q);
+    if (fr < 1e-9 || fr > 1.0 - 1e-9) q = __ddiv_rn(d, width);
+    return q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
+}
+
 // Per-lane decode phases.  UNR = independent arcs per thread per emit batch.
 template <int UNR>
 struct Lane {
-    static constexpr int WUNR = 4;   // candidates per thread per winners batch
+    static constexpr int WUNR = UNR; // candidates per thread per winners batch
     static constexpr int AUNR = 2;   // touched states per thread per aggregate batch
     static constexpr int EUNR = 2;   // frontier entries per thread per epsilon batch
     const GraphDev &g;      // __grid_constant__ kernel parameters: referenced in place,
@@ -226,24 +246,25 @@ struct Lane {
     const LaneWs &L;
     const UttDesc &io;
     const Grp G;
-    double *acrow;          // shared-memory row (when p.acrow_smem)
-    int *own_base;          // per-warp arc-slot owner maps (WMAP ints per warp, shared memory)
-    char *scratch_base;     // per-warp phase scratch (WSCR bytes per warp, shared memory)
-    int *whist_base;        // per-warp max-active histograms (NBINS ints per warp, shared memory)
     unsigned long long *wprof = nullptr;   // per-warp busy-time accumulators (profiling only)
     const double *row;      // global row of the current frame
     int par;                // parity of the current frame (counter set)
 
-    // Dynamic shared memory: [acrow: D f64 when p.acrow_smem][owner maps][stages][histograms]
+    // Dynamic shared memory (lane_dyn): [acrow: D f64 when p.acrow_smem][owner maps]
+    // [per-warp scratch][per-warp histograms].  Addresses are derived from the
+    // namespace-scope shared array at each use so they stay shared::cta.
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
-                    const Grp &G_, double *dyn)
-        : g(g_), p(p_), L(L_), io(io_), G(G_), acrow(dyn), row(nullptr), par(0) {
-        const int nw = blockDim.x >> 5;
-        own_base = reinterpret_cast<int *>(dyn + (p.acrow_smem ? p.D : 0));
-        scratch_base = reinterpret_cast<char *>(own_base + nw * WMAP);
-        whist_base = reinterpret_cast<int *>(scratch_base + nw * WSCR);
+                    const Grp &G_, double *)
+        : g(g_), p(p_), L(L_), io(io_), G(G_), row(nullptr), par(0) {}
+    __device__ __forceinline__ int acrow_doubles() const { return p.acrow_smem ? p.D : 0; }
+    __device__ __forceinline__ int *own_all() const { return reinterpret_cast<int *>(lane_dyn + acrow_doubles()); }
+    __device__ __forceinline__ char *scratch_all() const {
+        return reinterpret_cast<char *>(own_all() + (blockDim.x >> 5) * WMAP);
     }
-    __device__ __forceinline__ char *scratch() const { return scratch_base + (threadIdx.x >> 5) * WSCR; }
+    __device__ __forceinline__ int *whist_all() const {
+        return reinterpret_cast<int *>(scratch_all() + (blockDim.x >> 5) * WSCR);
+    }
+    __device__ __forceinline__ char *scratch() const { return scratch_all() + (threadIdx.x >> 5) * WSCR; }
     // u32 stage q (0, 1) of this warp's scratch (winners)
     __device__ __forceinline__ WStage stage(int q) const {
         WStage st;
@@ -272,10 +293,10 @@ struct Lane {
     }
     __device__ __forceinline__ EpsWin *rpk(int r) const { return L.rpk + (size_t)(r & 1) * L.S; }
     __device__ __forceinline__ unsigned *fixes() const { return L.fix + (size_t)G.rank * L.S; }
-    __device__ __forceinline__ int *wmap() const { return own_base + (threadIdx.x >> 5) * WMAP; }
+    __device__ __forceinline__ int *wmap() const { return own_all() + (threadIdx.x >> 5) * WMAP; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
-        return p.acrow_smem ? acrow[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
+        return p.acrow_smem ? lane_dyn[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
     }
 
     __device__ __forceinline__ void set_error(int code, int frame, long long aux) const {
@@ -288,7 +309,7 @@ struct Lane {
     __device__ void load_row(const double *r) {
         row = r;
         if (p.acrow_smem)
-            for (int d = threadIdx.x; d < p.D; d += blockDim.x) acrow[d] = __dmul_rn(__ldg(r + d), p.scale);
+            for (int d = threadIdx.x; d < p.D; d += blockDim.x) lane_dyn[d] = __dmul_rn(__ldg(r + d), p.scale);
     }
 
     // Clear the counter set of the NEXT frame (its previous readers are done).
@@ -296,8 +317,8 @@ struct Lane {
         const int q = par ^ 1;
         if (G.leader()) G.M->ntok[q] = G.M->nlat[q] = 0;
         if (threadIdx.x == 0) {
-            G.S->ntouched[q] = G.S->ncand[q] = G.S->nseed[q] = G.S->nfix[q] = 0;
-            G.S->best[q] = SENT;
+            lane_sm.ntouched[q] = lane_sm.ncand[q] = lane_sm.nseed[q] = lane_sm.nfix[q] = 0;
+            lane_sm.best[q] = SENT;
         }
     }
 
@@ -316,16 +337,16 @@ struct Lane {
     __device__ double emit(const unsigned *pts, const double *ptc, int np, double beam_eff, int frame) {
         StateRec *rec = L.rec;
         unsigned c_scan = 0, c_cand = 0;
-        int *ncand = &G.S->ncand[par];
+        int *ncand = &lane_sm.ncand[par];
         int4 *cb = L.cand + (size_t)G.rank * L.ccap;
         int *cbi = L.candi + (size_t)G.rank * L.ccap;
         const long long ccap = L.ccap;
-        unsigned long long *run = &G.S->best[par];
+        unsigned long long *run = &lane_sm.best[par];
         const int lane = threadIdx.x & 31;
         const unsigned lt = (1u << lane) - 1u;
         int cstart = 0, cused = CCH;          // current chunk (warp-uniform); none yet
         bool overflow = false;
-        if (threadIdx.x == 0) G.S->nfr[0] = G.S->nfr[1] = G.S->nfr[2] = 0;
+        if (threadIdx.x == 0) lane_sm.nfr[0] = lane_sm.nfr[1] = lane_sm.nfr[2] = 0;
         const unsigned long long t0 = wbegin();
         auto fill_tail = [&]() {
             for (int i = cused + lane; i < CCH; i += 32) __stcg(cb + cstart + i, make_int4(-1, 0, 0, 0));
@@ -408,8 +429,8 @@ struct Lane {
         c_cand = warp_sum(c_cand);
         c_scan = warp_sum(c_scan);
         if (lane == 0) {
-            atomicAdd(&G.S->c_cand, (unsigned long long)c_cand);
-            atomicAdd(&G.S->c_scan, (unsigned long long)c_scan);
+            atomicAdd(&lane_sm.c_cand, (unsigned long long)c_cand);
+            atomicAdd(&lane_sm.c_scan, (unsigned long long)c_scan);
         }
         wend(0, t0);
         G.sync();
@@ -427,7 +448,7 @@ struct Lane {
     // are not rewritten before this frame's aggregate.  `fpar` = previous frame's
     // parity (its fix count), `tbf`/`nf` = its token list.
     __device__ void fix_preds(int fpar, int frame, long long tbf, int nf) {
-        const int mine = G.S->nfix[fpar];
+        const int mine = lane_sm.nfix[fpar];
         const unsigned *fx = fixes();
         for (int q = threadIdx.x; q < mine; q += blockDim.x) {
             const long long o = tbf + (long long)__ldcg(fx + q);
@@ -446,23 +467,45 @@ struct Lane {
     // plain read-modify-write) and is summed into the CTA histogram at the end,
     // so no shared-memory atomic is ever contended.
     __device__ void winners(double cutoff, double best) {
-        const int nc = G.S->ncand[par];
+        const int nc = lane_sm.ncand[par];
         const bool hist = p.max_active > 0;
         const double width = __ddiv_rn(p.beam, (double)NBINS);
+        const double inv_w = __drcp_rn(width);
         const int4 *cb = L.cand + (size_t)G.rank * L.ccap;
         const int *cbi = L.candi + (size_t)G.rank * L.ccap;
         StateRec *rec = L.rec;
         unsigned *tl = touched();
         unsigned *f0 = front(0);
-        int *ntouched = &G.S->ntouched[par], *nf0 = &G.S->nfr[0];
+        int *ntouched = &lane_sm.ntouched[par], *nf0 = &lane_sm.nfr[0];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        int *wh = whist_base + warp * NBINS;
+        int *wh = whist_all() + warp * NBINS;
         if (hist)
             for (int b = lane; b < NBINS; b += 32) wh[b] = 0;
         __syncwarp();
         WStage st_t = stage(0), st_f = stage(1);
         unsigned nseed = 0;
         const unsigned long long t0 = wbegin();
+        if (p.exp & 4) {   // timing probe: the loop's loads and owner test only
+            unsigned nown = 0;
+            for (int kb = warp * 32 * WUNR; kb < nc; kb += nw * 32 * WUNR) {
+                int4 e[WUNR];
+#pragma unroll
+                for (int u = 0; u < WUNR; u++) {
+                    const int k = kb + u * 32 + lane;
+                    e[u].x = -1;
+                    if (k < nc) e[u] = __ldcg(cb + k);
+                }
+                unsigned long long pk[WUNR];
+#pragma unroll
+                for (int u = 0; u < WUNR; u++)
+                    pk[u] = e[u].x != -1 ? __ldcg(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
+#pragma unroll
+                for (int u = 0; u < WUNR; u++)
+                    nown += e[u].x != -1 && pk[u] == pack_word(__hiloint2double(e[u].w, e[u].z), (unsigned)e[u].y);
+            }
+            if (nown == 0xFFFFFFFFu) lane_sm.err_aux = nown;
+            if (p.exp & 8) { wend(2, t0); return; }
+        }
         for (int kb = warp * 32 * WUNR; kb < nc; kb += nw * 32 * WUNR) {
             int4 e[WUNR];
             int ti[WUNR];
@@ -490,34 +533,20 @@ struct Lane {
                 nseed += seed;
                 // only states with epsilon arcs enter the closure
                 st_f.push(seed && ((unsigned)e[u].x & EPS_FLAG), v, nf0, f0);
-                if (hist) {
-                    int bin = NBINS + lane;       // unique dummy key for non-seeds
-                    if (seed) {
-                        const double q = (p.exp & 1) ? __dmul_rn(__dsub_rn(cand, best), 1.0 / width)
-                                                     : __ddiv_rn(__dsub_rn(cand, best), width);
-                        bin = q >= (double)NBINS ? NBINS - 1 : (q < 0.0 ? 0 : (int)q);
-                    }
-                    if (p.exp & 2) {
-                        if (seed) atomicAdd(wh + bin, 1);
-                    } else {
-                        const unsigned grp = __match_any_sync(FULL, bin);
-                        if (seed && lane == __ffs(grp) - 1) wh[bin] += __popc(grp);
-                        __syncwarp();
-                    }
-                }
+                if (hist && seed) atomicAdd(wh + hist_bin(cand, best, width, inv_w), 1);
             }
         }
         st_t.flush(ntouched, tl);
         st_f.flush(nf0, f0);
         nseed = warp_sum(nseed);
-        if (lane == 0 && nseed) atomicAdd(&G.S->nseed[par], (int)nseed);
+        if (lane == 0 && nseed) atomicAdd(&lane_sm.nseed[par], (int)nseed);
         wend(1, t0);
         if (hist) {
             __syncthreads();
             for (int b = threadIdx.x; b < NBINS; b += blockDim.x) {
                 int sum = 0;
-                for (int w = 0; w < nw; w++) sum += whist_base[w * NBINS + b];
-                G.S->hist[par][b] = sum;
+                for (int w = 0; w < nw; w++) sum += whist_all()[w * NBINS + b];
+                lane_sm.hist[par][b] = sum;
             }
         }
     }
@@ -570,10 +599,10 @@ struct Lane {
                 const double h = __dadd_rn(best, __dmul_rn((double)(bstar < 1 ? 1 : bstar), width));
                 c2 = h < cutoff ? h : cutoff;
             }
-            if (lane == 0) G.S->red0 = c2;
+            if (lane == 0) lane_sm.red0 = c2;
         }
         __syncthreads();
-        const double r = G.S->red0;
+        const double r = lane_sm.red0;
         __syncthreads();
         return r;
     }
@@ -589,10 +618,10 @@ struct Lane {
     __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
         StateRec *rec = L.rec;
-        unsigned round_id = G.S->round_id;
+        unsigned round_id = lane_sm.round_id;
         unsigned c_escan = 0, c_ecand = 0, c_front = 0;
         unsigned *tl = touched();
-        int *ntouched = &G.S->ntouched[par];
+        int *ntouched = &lane_sm.ntouched[par];
         const int bd = blockDim.x;
         bool ok = true;
         for (int r = 0;; r++) {
@@ -605,11 +634,11 @@ struct Lane {
                 break;
             }
             ++round_id;
-            const int nf = G.S->nfr[r % 3];
+            const int nf = lane_sm.nfr[r % 3];
             const unsigned *fs = front(r);
             unsigned *fsn = front(r + 1);
-            int *nnext = &G.S->nfr[(r + 1) % 3];
-            if (threadIdx.x == 0) G.S->nfr[(r + 2) % 3] = 0;   // read at round r-1's start, one barrier ago
+            int *nnext = &lane_sm.nfr[(r + 1) % 3];
+            if (threadIdx.x == 0) lane_sm.nfr[(r + 2) % 3] = 0;   // read at round r-1's start, one barrier ago
             EpsWin *rprev = rpk(r + 1);                         // == rpk(r - 1)
             EpsWin *rcur = rpk(r);
             const unsigned long long t0 = wbegin();
@@ -653,14 +682,14 @@ struct Lane {
                         c_ecand++;
                         const unsigned x = (unsigned)rr.x;
                         const unsigned long long word = pack_word(cand, (unsigned)rr.y);
-                        const unsigned long long old = atomicMin(&rec[x].pack, word);
+                        const unsigned long long old = atom_min_u64(&rec[x].pack, word);
                         if (old == SENT) {
                             const int sl = agg_append(ntouched);
                             __stcg(tl + sl, x);
                         }
                         if (old > word) {
                             epswin_min(rcur + x, word, cand);
-                            if (atomicExch(L.tag + x, round_id) != round_id) {
+                            if (atom_exch_u32(L.tag + x, round_id) != round_id) {
                                 const int sl = agg_append(nnext);
                                 __stcg(fsn + sl, x);
                             }
@@ -675,11 +704,11 @@ struct Lane {
         c_ecand = warp_sum(c_ecand);
         c_front = warp_sum(c_front);
         if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&G.S->c_escan, (unsigned long long)c_escan);
-            atomicAdd(&G.S->c_ecand, (unsigned long long)c_ecand);
-            atomicAdd(&G.S->c_front, (unsigned long long)c_front);
+            atomicAdd(&lane_sm.c_escan, (unsigned long long)c_escan);
+            atomicAdd(&lane_sm.c_ecand, (unsigned long long)c_ecand);
+            atomicAdd(&lane_sm.c_front, (unsigned long long)c_front);
         }
-        if (threadIdx.x == 0) G.S->round_id = round_id;
+        if (threadIdx.x == 0) lane_sm.round_id = round_id;
         if (!ok) G.sync();
         return ok;
     }
@@ -747,14 +776,14 @@ struct Lane {
             } else if (i < st.n) {
                 __stcg(&rec[st.v[i]].pack, SENT);   // over the arena: error raised after the barrier
             }
-            sf.push(fx, (unsigned)idx, &G.S->nfix[par], fixes());
+            sf.push(fx, (unsigned)idx, &lane_sm.nfix[par], fixes());
         }
         __syncwarp();
         st.n = 0;
     }
 
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = G.S->ntouched[par];
+        const int nt = lane_sm.ntouched[par];
         const long long room = io.tok_cap - tb;
         StateRec *rec = L.rec;
         const unsigned *tl = touched();
@@ -795,7 +824,7 @@ struct Lane {
             }
         }
         flush_tokens(st, sf, frame, tb, room);
-        sf.flush(&G.S->nfix[par], fixes());
+        sf.flush(&lane_sm.nfix[par], fixes());
         wend(4, t0);
         G.sync();
         const int n = G.M->ntok[par];
@@ -874,7 +903,7 @@ struct Lane {
     // ---- error path: O(touched) reset of every per-state word this frame touched ----
     __device__ void reset_touched() {
         G.sync();
-        const int nt = G.S->ntouched[par];
+        const int nt = lane_sm.ntouched[par];
         const unsigned *tl = touched();
         const double inf = inf_d();
         for (int k = threadIdx.x; k < nt; k += blockDim.x) {
@@ -888,7 +917,8 @@ struct Lane {
     }
 };
 
-__device__ __forceinline__ void init_smem(Smem &sm, unsigned round_ctr) {
+__device__ __forceinline__ void init_smem(unsigned round_ctr) {
+    Smem &sm = lane_sm;
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; q++) {
             sm.ntok[q] = sm.nlat[q] = 0;
@@ -912,10 +942,10 @@ __device__ __forceinline__ void seed_start(Lane<UNR> &ln, const GraphDev &g, con
         __stcg(&r->cost, 0.0);
         __stcg(&r->pred, -1);
         __stcg(ln.touched(), (unsigned)g.start);
-        ln.G.S->ntouched[0] = 1;
+        lane_sm.ntouched[0] = 1;
         if (g.has_eps) {
             __stcg(ln.front(0), (unsigned)g.start);
-            ln.G.S->nfr[0] = 1;
+            lane_sm.nfr[0] = 1;
         }
     }
 }
@@ -929,22 +959,20 @@ template <int NT, int UNR, bool LAT, bool PROF>
 __global__ void __launch_bounds__(NT, 1)
 decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
               const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts, int n_utts) {
-    __shared__ Smem sm;
-    extern __shared__ double s_acrow[];
+    Smem &sm = lane_sm;
     cgx::cluster_group cl = cgx::this_cluster();
     Grp G;
     G.C = (int)cl.num_blocks();
     G.rank = (int)cl.block_rank();
-    G.S = &sm;
     G.M = cl.map_shared_rank(&sm, 0);
     const int u_idx = blockIdx.x / G.C;      // uniform across the cluster
     if (u_idx >= n_utts) return;
     const LaneWs &L = lanes[u_idx];
     const UttDesc &io = utts[u_idx];
-    init_smem(sm, __ldcg(L.round_ctr));
+    init_smem(__ldcg(L.round_ctr));
     G.sync();
 
-    Lane<UNR> ln(g, p, L, io, G, s_acrow);
+    Lane<UNR> ln(g, p, L, io, G, lane_dyn);
     if (PROF) ln.wprof = p.prof + 8;
     const int T = io.T;
     const double inf = inf_d();
@@ -1272,17 +1300,15 @@ __global__ void __launch_bounds__(768, 1)
 expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
               const __grid_constant__ LaneWs L, const __grid_constant__ UttDesc io, int n, int mode,
               double cutoff_in) {
-    __shared__ Smem sm;
-    extern __shared__ double s_acrow[];
+    Smem &sm = lane_sm;
     Grp G;
     G.C = 1;
     G.rank = 0;
-    G.S = &sm;
     G.M = cgx::this_cluster().map_shared_rank(&sm, 0);
     const int tid = threadIdx.x;
-    init_smem(sm, __ldcg(L.round_ctr));
+    init_smem(__ldcg(L.round_ctr));
     __syncthreads();
-    Lane<2> ln(g, p, L, io, G, s_acrow);
+    Lane<2> ln(g, p, L, io, G, lane_dyn);
     double cutoff = cutoff_in;
     ln.par = 1;
     if (mode == 0) {
