@@ -65,6 +65,8 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-utts", type=int, default=0)
     p.add_argument("--cpu-frames", type=int, default=100)
+    p.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C3 side measurements")
+    p.add_argument("--all-configs", action="store_true", help="also measure C5 (builds the 50M-arc graph)")
     return p.parse_args(argv)
 
 
@@ -218,6 +220,41 @@ def run_reference(args, dist: Dist):
     dist.close()
 
 
+def measure_configs(graph_c2, all_configs: bool) -> dict:
+    """Frames/s of the other BASELINE.json configs through the public API
+    (host numpy costs in, DecodeResult out; one warm-up call, one timed call).
+    C1: uniform 10k x 5 graph, 20 utterances x 300 frames, 1-best + lattice.
+    C2: C2 HCLG, one utterance (one lane: the single-stream latency case).
+    C3: C2 + exact lattice generation, pruning and finalisation.
+    C5: the 50M-arc stress graph (only with --all-configs: it takes ~15 s to build)."""
+    import paper_1804_03243_b200 as lb
+    from paper_1804_03243_b200 import synthetic
+
+    def run(name, graph, n_utts, want_lattice):
+        d = synthetic.CONFIGS[name]["decode"]
+        mats = [np.ascontiguousarray(synthetic.config_matrix(name, u).costs) for u in range(n_utts)]
+        cfg = lb.DecodeConfig(beam=d["beam"], lattice_beam=d["lattice_beam"], max_active=d["max_active"],
+                              max_lattice_arcs=50_000_000)
+        lb.decode_batch(graph, mats, cfg, want_lattice=want_lattice)
+        t0 = time.perf_counter()
+        res = lb.decode_batch(graph, mats, cfg, want_lattice=want_lattice)
+        dt = time.perf_counter() - t0
+        frames = sum(m.shape[0] for m in mats)
+        out = {"frames_per_s": frames / dt, "utterances": n_utts, "frames": frames, "seconds": dt,
+               "want_lattice": want_lattice}
+        if want_lattice:
+            out["lattice_arcs"] = int(sum(r.lattice.num_arcs for r in res))
+        return out
+
+    res = {"C1": run("C1", synthetic.config_graph("C1"), 20, True),
+           "C2": run("C2", graph_c2, 1, False),
+           "C3": run("C3", graph_c2, 1, True)}
+    if all_configs:
+        res["C5"] = run("C5", synthetic.config_graph("C5"), 1, False)
+    res["note"] = "public API decode_batch, host costs, wall clock incl. H2D/D2H and host result assembly"
+    return res
+
+
 def config_dict(args, note=""):
     d = {"workload": "C4: sequence-parallel batch on the C2 HCLG graph (1-best, beam 13, max-active 7000)",
          "graph": f"hclg_graph(seed=0, states={args.states}), 3000 pdfs, acyclic epsilon depth<=4",
@@ -336,6 +373,10 @@ def main(argv=None):
                 "step_host_ms": host_ms / max(args.steps, 1),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
 
+    configs = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_configs:
+        configs = measure_configs(graph, args.all_configs)
+
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         from oracle import oracle as O
@@ -351,7 +392,7 @@ def main(argv=None):
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic", "arcs_per_sec": arcs_all / (t_max / 1e3),
                "config": config_dict(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": launches, "clocks": ck}
+               "gpu_launches": launches, "clocks": ck, "configs_measured": configs}
         print(json.dumps(out), flush=True)
     dist.close()
 

@@ -49,6 +49,7 @@ typedef struct {
     int32_t lanes;                /* concurrent utterances per launch (CTAs); 0 = auto */
     int32_t threads_per_lane;     /* CTA size: 512 or 768; 0 = auto (768) */
     int32_t ctas_per_lane;        /* thread-block cluster size of a lane (1..4); 0 = auto */
+    int32_t keep_work_lattice;    /* also keep every live arc + extra (DecodeResult.work_lattice) */
 } lb_config;
 
 int32_t lb_version(void);
@@ -92,9 +93,20 @@ int lb_result_path(const lb_result *r, int32_t utt, int32_t *arcs);
 int lb_result_tokens(const lb_result *r, int32_t utt, int64_t *frame_off, int32_t *states,
                      double *costs, int32_t *pred_arc, int32_t *pred_idx, uint64_t *packs);
 /* Live lattice arcs per block with their pruning extra cost (lattice.py:473-497);
- * from/to index the device-order token lists of the arc's frames. */
+ * from/to index the device-order token lists of the arc's frames.  Needs
+ * keep_work_lattice. */
 int lb_result_lattice(const lb_result *r, int32_t utt, int64_t *block_off, int32_t *arc,
                       int32_t *from_idx, int32_t *to_idx, double *extra);
+/* Final lattice of a want_lattice decode, finalised on the device
+ * (finalize_lattice, lattice.py:537-598): sizes, then the arrays.  node_keys
+ * are (frame << 32) | index into the frame's state-sorted token list, ascending
+ * (node id = position); arcs are in canonical order (from, to, ilabel,
+ * olabel, graph_cost, acoustic_cost). */
+int lb_result_final_lattice(const lb_result *r, int32_t utt, int64_t *num_nodes, int64_t *start,
+                            int64_t *n_final, int64_t *n_arcs);
+int lb_result_final_arrays(const lb_result *r, int32_t utt, uint64_t *node_keys, int64_t *final_ids,
+                           double *final_costs, int32_t *from, int32_t *to, int32_t *ilabel,
+                           int32_t *olabel, double *graph_cost, double *acoustic_cost);
 /* counters[8]: tokens expanded, arcs scanned, emitting candidates, epsilon
  * frontier entries, epsilon arcs scanned, epsilon candidates, tokens kept,
  * lattice arcs. */
@@ -113,6 +125,14 @@ int lb_result_phases(const lb_result *r, double *ms8);
  * from waiting on the slowest warp. */
 int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8);
 void lb_result_free(lb_result *r);
+
+/* write_lattice_text (lattice.py:605-614) in native code, byte-identical to the
+ * reference's text (floats as Python repr): returns the text length; the text
+ * is written to buf only if cap >= that length.  Host-only, no device needed. */
+int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const int64_t *final_ids,
+                        const double *final_costs, int64_t n_arcs, const int64_t *from, const int64_t *to,
+                        const int64_t *ilabel, const int64_t *olabel, const double *graph_cost,
+                        const double *acoustic_cost, char *buf, int64_t cap);
 
 /* Single-op surfaces (decoder.py:373-435): one frontier on device.
  * out_* need room for num_states entries; *n_out receives the count. */

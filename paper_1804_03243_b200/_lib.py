@@ -38,11 +38,15 @@ SIGNATURES = {
     "lb_result_tokens": (C.c_int, [PV, C.c_int32, P64, P32, PD, P32, P32, PU64]),
     "lb_result_lattice": (C.c_int, [PV, C.c_int32, P64, P32, P32, P32, PD]),
     "lb_result_counters": (C.c_int, [PV, C.c_int32, P64]),
+    "lb_result_final_lattice": (C.c_int, [PV, C.c_int32, P64, P64, P64, P64]),
+    "lb_result_final_arrays": (C.c_int, [PV, C.c_int32, PU64, P64, PD, P32, P32, P32, P32, PD, PD]),
     "lb_result_timing": (C.c_int, [PV, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                    C.POINTER(C.c_float), C.POINTER(C.c_float), P32]),
     "lb_result_phases": (C.c_int, [PV, PD]),
     "lb_result_warp_phases": (C.c_int, [PV, PD, PD]),
     "lb_result_free": (None, [PV]),
+    "lb_lattice_text": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64, P64, PD, C.c_int64, P64, P64, P64,
+                                    P64, PD, PD, C.c_char_p, C.c_int64]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,
                                      P64, PD]),
     "lb_expand_nonemitting": (C.c_int, [PV, P32, PD, C.c_int64, C.c_double, P32, PD, P64]),
@@ -54,10 +58,20 @@ class LbConfig(C.Structure):
                 ("max_active", C.c_int64), ("max_tokens_per_frame", C.c_int64),
                 ("max_lattice_arcs", C.c_int64), ("token_arena", C.c_int64),
                 ("want_lattice", C.c_int32), ("collect_frame_packs", C.c_int32),
-                ("lanes", C.c_int32), ("threads_per_lane", C.c_int32), ("ctas_per_lane", C.c_int32)]
+                ("lanes", C.c_int32), ("threads_per_lane", C.c_int32), ("ctas_per_lane", C.c_int32),
+                ("keep_work_lattice", C.c_int32)]
 
 
 _lib = None
+_host_lib = None
+
+
+def host_lib():
+    """The library bound for host-only entry points (no device required)."""
+    global _host_lib
+    if _host_lib is None:
+        _host_lib = load_symbols_only()
+    return _host_lib
 
 
 def load_symbols_only():

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -17,6 +18,7 @@
 
 #include "../../include/latbeam_b200.h"
 #include "lb_kernels.cuh"
+#include "lb_lattice.cuh"
 
 using namespace lbk;
 
@@ -53,6 +55,34 @@ struct UttHost {
     std::vector<int32_t> states, pred_arc, pred_idx, larc, lfrom, lto;
     std::vector<double> costs, lextra;
     std::vector<uint64_t> packs;
+    // final lattice (device-finalised, lattice.py:500-598)
+    bool has_final = false;
+    int64_t fl_start = -1;
+    std::vector<uint64_t> fl_nodes;        // (frame << 32) | state-sorted index, ascending
+    std::vector<int64_t> fl_final_ids;
+    std::vector<double> fl_final_costs;
+    std::vector<int32_t> fl_from, fl_to, fl_il, fl_ol;
+    std::vector<double> fl_g, fl_ac;
+};
+
+// Growable device scratch of the lattice finaliser.
+struct FlScratch {
+    std::vector<void *> bufs;
+    size_t tok_cap = 0, arc_cap = 0, temp_cap = 0;
+    unsigned long long *keys0 = nullptr, *keys1 = nullptr, *fk = nullptr, *tk = nullptr, *nodes0 = nullptr,
+                       *nodes1 = nullptr, *k64a = nullptr, *k64b = nullptr, *count = nullptr;
+    int *idx0 = nullptr, *idx1 = nullptr, *rank = nullptr, *perm0 = nullptr, *perm1 = nullptr;
+    unsigned *il = nullptr, *ol = nullptr, *fid = nullptr, *tid = nullptr, *k32a = nullptr, *k32b = nullptr;
+    double *gc = nullptr, *ac = nullptr, *o_g = nullptr, *o_ac = nullptr, *fcs = nullptr;
+    long long *surv = nullptr, *start_rank = nullptr, *fids = nullptr;
+    int *o_from = nullptr, *o_to = nullptr, *o_il = nullptr, *o_ol = nullptr, *n_unique = nullptr;
+    void *temp = nullptr;
+    void release() {
+        for (void *p : bufs) cudaFree(p);
+        bufs.clear();
+        tok_cap = arc_cap = temp_cap = 0;
+    }
+    ~FlScratch() { release(); }
 };
 
 // Per-graph reusable device workspace: lane scratch (O(S) per lane, per-CTA
@@ -349,17 +379,148 @@ int validate_cfg(const lb_config *c) {
     if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
     if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
     if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
-    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 640 &&
-        c->threads_per_lane != 768)
-        return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
+    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 768)
+        return set_err(LB_USAGE, "threads_per_lane must be 512 or 768");
     if (c->ctas_per_lane < 0 || c->ctas_per_lane > 4) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 4]");
+    return LB_OK;
+}
+
+// Device lattice finalisation of one utterance (lb_lattice.cuh); fills u.fl_*.
+// Returns LB_OK, or an LB_* status for CUDA failures; reference DecodeFailures
+// (no surviving arc / start not connected / no terminal node) go to u.status.
+int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, double lattice_beam, int partial,
+                    FlScratch &sc, cudaStream_t st, UttHost &u) {
+    long long tb[2], lbase[2];
+    CK(cudaMemcpyAsync(&tb[0], d.tok_base + T + 1, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&lbase[0], d.lat_base + T + 1, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const long long ntok = tb[0], nlat = lbase[0];
+    const int nblk = g->sms * 4;
+    auto grow = [&](auto **p, size_t n) -> cudaError_t {
+        cudaError_t e = dalloc(p, n);
+        if (e == cudaSuccess) sc.bufs.push_back((void *)*p);
+        return e;
+    };
+    if ((size_t)ntok > sc.tok_cap || (size_t)nlat > sc.arc_cap || !sc.count) {
+        sc.release();
+        sc.tok_cap = std::max<size_t>(ntok, 1024);
+        sc.arc_cap = std::max<size_t>(nlat, 1024);
+        const size_t nt = sc.tok_cap, na = sc.arc_cap;
+        CK(grow(&sc.keys0, nt)); CK(grow(&sc.keys1, nt)); CK(grow(&sc.idx0, nt)); CK(grow(&sc.idx1, nt));
+        CK(grow(&sc.rank, nt));
+        CK(grow(&sc.surv, na)); CK(grow(&sc.fk, na)); CK(grow(&sc.tk, na)); CK(grow(&sc.il, na)); CK(grow(&sc.ol, na));
+        CK(grow(&sc.gc, na)); CK(grow(&sc.ac, na)); CK(grow(&sc.nodes0, 2 * na)); CK(grow(&sc.nodes1, 2 * na));
+        CK(grow(&sc.fid, na)); CK(grow(&sc.tid, na)); CK(grow(&sc.perm0, na)); CK(grow(&sc.perm1, na));
+        CK(grow(&sc.k64a, na)); CK(grow(&sc.k64b, na)); CK(grow(&sc.k32a, na)); CK(grow(&sc.k32b, na));
+        CK(grow(&sc.o_from, na)); CK(grow(&sc.o_to, na)); CK(grow(&sc.o_il, na)); CK(grow(&sc.o_ol, na));
+        CK(grow(&sc.o_g, na)); CK(grow(&sc.o_ac, na)); CK(grow(&sc.fids, 2 * na)); CK(grow(&sc.fcs, 2 * na));
+        CK(grow(&sc.count, 4)); CK(grow(&sc.start_rank, 1)); CK(grow(&sc.n_unique, 1));
+        // CUB temp storage for the largest sort / unique of this capacity
+        size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, sc.keys0, sc.keys1, sc.idx0, sc.idx1, (int)nt, 0, 64, st));
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, t2, sc.nodes0, sc.nodes1, (int)(2 * na), 0, 64, st));
+        CK(cub::DeviceSelect::Unique(nullptr, t3, sc.nodes1, sc.nodes0, sc.n_unique, (int)(2 * na), st));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, t4, sc.k64a, sc.k64b, sc.perm0, sc.perm1, (int)na, 0, 64, st));
+        sc.temp_cap = std::max(std::max(t1, t2), std::max(t3, t4));
+        CK(grow((char **)&sc.temp, sc.temp_cap));
+    }
+    size_t tcap = sc.temp_cap;
+    const int nfr = T + 1;
+    // 1-2: state-sorted token ranks per frame
+    fl_token_keys<<<nblk, 256, 0, st>>>(d.tok_state, d.tok_base, nfr, ntok, sc.keys0, sc.idx0);
+    CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.keys0, sc.keys1, sc.idx0, sc.idx1, (int)ntok, 0, 64, st));
+    CK(cudaMemsetAsync(sc.start_rank, 0xFF, 8, st));
+    fl_token_rank<<<nblk, 256, 0, st>>>(sc.keys1, sc.idx1, d.tok_base, ntok, g->start, sc.rank, sc.start_rank);
+    // 3: survivors
+    CK(cudaMemsetAsync(sc.count, 0, 32, st));
+    fl_survivors<<<nblk, 256, 0, st>>>(d.lat_extra, nlat, lattice_beam, sc.surv, sc.count);
+    unsigned long long m = 0;
+    long long start_rank = -1;
+    CK(cudaMemcpyAsync(&m, sc.count, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&start_rank, sc.start_rank, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    u.has_final = true;
+    if (m == 0) {
+        u.status = LB_DECODE_FAILURE;
+        u.msg = "no lattice arcs survived pruning";
+        return LB_OK;
+    }
+    // 4: arc fields + node keys, sorted unique nodes, dense ids
+    fl_arc_fields<<<nblk, 256, 0, st>>>(g->dev(), sc.surv, (long long)m, d.lat_arc, d.lat_from, d.lat_to, d.lat_base,
+                                        d.tok_base, nfr, sc.rank, d.costs, D, scale, sc.fk, sc.tk, sc.il, sc.ol, sc.gc,
+                                        sc.ac, sc.nodes0);
+    CK(cub::DeviceRadixSort::SortKeys(sc.temp, tcap, sc.nodes0, sc.nodes1, (int)(2 * m), 0, 64, st));
+    CK(cub::DeviceSelect::Unique(sc.temp, tcap, sc.nodes1, sc.nodes0, sc.n_unique, (int)(2 * m), st));
+    int nn = 0;
+    CK(cudaMemcpyAsync(&nn, sc.n_unique, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fl_node_ids<<<nblk, 256, 0, st>>>(sc.fk, sc.tk, (long long)m, sc.nodes0, nn, sc.fid, sc.tid);
+    // 5: canonical order = np.lexsort((ac, g, ol, il, to, from)): stable LSD passes, last key primary
+    fl_iota<<<nblk, 256, 0, st>>>(sc.perm0, (long long)m);
+    int *pa = sc.perm0, *pb = sc.perm1;
+    for (int pass = 0; pass < 6; pass++) {
+        if (pass < 2) {
+            fl_gather_u64<<<nblk, 256, 0, st>>>(pass == 0 ? sc.ac : sc.gc, pa, (long long)m, sc.k64a);
+            CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.k64a, sc.k64b, pa, pb, (int)m, 0, 64, st));
+        } else {
+            const unsigned *src = pass == 2 ? sc.ol : pass == 3 ? sc.il : pass == 4 ? sc.tid : sc.fid;
+            fl_gather_u32<<<nblk, 256, 0, st>>>(src, pa, (long long)m, sc.k32a);
+            CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.k32a, sc.k32b, pa, pb, (int)m, 0, 32, st));
+        }
+        std::swap(pa, pb);
+    }
+    fl_emit<<<nblk, 256, 0, st>>>(pa, (long long)m, sc.fid, sc.tid, sc.il, sc.ol, sc.gc, sc.ac, sc.o_from, sc.o_to,
+                                  sc.o_il, sc.o_ol, sc.o_g, sc.o_ac);
+    // 6: final nodes
+    fl_finals<<<nblk, 256, 0, st>>>(sc.nodes0, nn, T, sc.keys1, d.tok_base, g->fin, partial, sc.fids, sc.fcs,
+                                    sc.count + 1);
+    CK(cudaGetLastError());
+    unsigned long long nf = 0;
+    CK(cudaMemcpyAsync(&nf, sc.count + 1, 8, cudaMemcpyDeviceToHost, st));
+    u.fl_nodes.resize(nn);
+    u.fl_from.resize(m); u.fl_to.resize(m); u.fl_il.resize(m); u.fl_ol.resize(m); u.fl_g.resize(m); u.fl_ac.resize(m);
+    CK(cudaMemcpyAsync(u.fl_nodes.data(), sc.nodes0, 8 * (size_t)nn, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_from.data(), sc.o_from, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_to.data(), sc.o_to, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_il.data(), sc.o_il, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_ol.data(), sc.o_ol, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_g.data(), sc.o_g, 8 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_ac.data(), sc.o_ac, 8 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> ids(nf);
+    std::vector<double> fcs(nf);
+    CK(cudaMemcpy(ids.data(), sc.fids, 8 * nf, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fcs.data(), sc.fcs, 8 * nf, cudaMemcpyDeviceToHost));
+    std::vector<size_t> ord(nf);
+    for (size_t i = 0; i < nf; i++) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+    u.fl_final_ids.resize(nf);
+    u.fl_final_costs.resize(nf);
+    for (size_t i = 0; i < nf; i++) {
+        u.fl_final_ids[i] = ids[ord[i]];
+        u.fl_final_costs[i] = fcs[ord[i]];
+    }
+    // start node (frame 0, the start token's rank)
+    const uint64_t sk = (uint64_t)(start_rank < 0 ? 0 : start_rank);
+    auto it = std::lower_bound(u.fl_nodes.begin(), u.fl_nodes.end(), sk);
+    if (start_rank < 0 || it == u.fl_nodes.end() || *it != sk) {
+        u.status = LB_DECODE_FAILURE;
+        u.msg = "surviving arcs do not connect to the start node";
+        return LB_OK;
+    }
+    u.fl_start = it - u.fl_nodes.begin();
+    if (nf == 0) {
+        u.status = LB_DECODE_FAILURE;
+        u.msg = "no terminal node survived pruning";
+    }
     return LB_OK;
 }
 
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms) {
     const bool lat = cfg->want_lattice != 0;
-    const bool packs = cfg->collect_frame_packs != 0 || lat;
+    const bool keep_work = lat && cfg->keep_work_lattice != 0;
+    const bool packs = cfg->collect_frame_packs != 0 || keep_work;
     int tmax = 1;
     for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
     const int64_t S = g->S;
@@ -425,9 +586,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
          : (prof ? decode_kernel<NT, U, false, true> : decode_kernel<NT, U, false, false>))
     KernT kern;
     if (threads == 768) kern = LB_PICK(768, 2);
-    else if (threads == 640) kern = LB_PICK(640, 4);
     else if (threads == 512) kern = LB_PICK(512, 4);
-    else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
+    else return set_err(LB_USAGE, "threads_per_lane must be 512 or 768");
 #undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();
@@ -439,6 +599,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     CK(cudaEventCreate(&e3));
     res->utts.resize(n);
     res->t_h2d = h2d_ms;
+    FlScratch fl;
     std::vector<UttDesc> desc(lanes);
     std::vector<int> hi(8 * lanes);
     std::vector<double> hd(4 * lanes);
@@ -497,7 +658,12 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             u.total_cost = hd[4 * l + 0];
             const int plen = hi[8 * l + 4];
             u.path.assign(hpath.begin() + (size_t)path_cap * l, hpath.begin() + (size_t)path_cap * l + plen);
-            if (packs || lat) {
+            if (lat) {
+                rc = finalize_device(g, desc[l], T[w0 + l], D, cfg->acoustic_scale, cfg->lattice_beam, u.partial, fl,
+                                     st, u);
+                if (rc) return rc;
+            }
+            if (packs || keep_work) {
                 const int Tu = T[w0 + l];
                 const UttDesc &d = desc[l];
                 u.frame_off.resize(Tu + 2);
@@ -517,7 +683,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
                     u.packs.resize(nt);
                     CK(cudaMemcpy(u.packs.data(), d.tok_pack, 8 * nt, cudaMemcpyDeviceToHost));
                 }
-                if (lat) {
+                if (keep_work) {
                     u.block_off.resize(Tu + 2);
                     CK(cudaMemcpy(u.block_off.data(), d.lat_base, sizeof(long long) * (Tu + 2), cudaMemcpyDeviceToHost));
                     const int64_t na = u.block_off[Tu + 1];
@@ -558,6 +724,46 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
 }  // namespace
 
 extern "C" {
+
+// Python repr() of a float (CPython float_repr_style 'short'): the shortest
+// round-trip digits; exponent form iff decpt <= -4 or decpt > 16; ".0" added to
+// integral fixed-form values.  Used by the lattice text writer so the native
+// output is byte-identical to write_lattice_text (lattice.py:605-614).
+static void py_repr(double x, std::string &out) {
+    if (std::isnan(x)) { out += "nan"; return; }
+    if (std::isinf(x)) { out += x < 0 ? "-inf" : "inf"; return; }
+    char b[64];
+    auto r = std::to_chars(b, b + sizeof b, x, std::chars_format::scientific);
+    std::string t(b, r.ptr);
+    size_t i = 0;
+    if (t[0] == '-') { out += '-'; i = 1; }
+    const size_t epos = t.find('e');
+    std::string digits;
+    for (size_t k = i; k < epos; k++)
+        if (t[k] != '.') digits += t[k];
+    const int e10 = std::atoi(t.c_str() + epos + 1);
+    const int decpt = e10 + 1;
+    const int nd = (int)digits.size();
+    if (decpt <= -4 || decpt > 16) {
+        out += digits[0];
+        if (nd > 1) { out += '.'; out.append(digits, 1, std::string::npos); }
+        char eb[16];
+        snprintf(eb, sizeof eb, "e%c%02d", e10 < 0 ? '-' : '+', e10 < 0 ? -e10 : e10);
+        out += eb;
+    } else if (decpt <= 0) {
+        out += "0.";
+        out.append((size_t)(-decpt), '0');
+        out += digits;
+    } else if (decpt >= nd) {
+        out += digits;
+        out.append((size_t)(decpt - nd), '0');
+        out += ".0";
+    } else {
+        out.append(digits, 0, (size_t)decpt);
+        out += '.';
+        out.append(digits, (size_t)decpt, std::string::npos);
+    }
+}
 
 int32_t lb_version(void) { return 1; }
 
@@ -863,6 +1069,35 @@ int lb_result_lattice(const lb_result *r, int32_t utt, int64_t *block_off, int32
     return LB_OK;
 }
 
+int lb_result_final_lattice(const lb_result *r, int32_t utt, int64_t *num_nodes, int64_t *start, int64_t *n_final,
+                            int64_t *n_arcs) {
+    UTT_OR_FAIL
+    if (!u.has_final) return set_err(LB_USAGE, "lattice was not requested");
+    if (num_nodes) *num_nodes = (int64_t)u.fl_nodes.size();
+    if (start) *start = u.fl_start;
+    if (n_final) *n_final = (int64_t)u.fl_final_ids.size();
+    if (n_arcs) *n_arcs = (int64_t)u.fl_from.size();
+    return LB_OK;
+}
+
+int lb_result_final_arrays(const lb_result *r, int32_t utt, uint64_t *node_keys, int64_t *final_ids,
+                           double *final_costs, int32_t *from, int32_t *to, int32_t *ilabel, int32_t *olabel,
+                           double *graph_cost, double *acoustic_cost) {
+    UTT_OR_FAIL
+    if (!u.has_final) return set_err(LB_USAGE, "lattice was not requested");
+    const size_t m = u.fl_from.size(), nf = u.fl_final_ids.size();
+    if (node_keys) std::memcpy(node_keys, u.fl_nodes.data(), 8 * u.fl_nodes.size());
+    if (final_ids) std::memcpy(final_ids, u.fl_final_ids.data(), 8 * nf);
+    if (final_costs) std::memcpy(final_costs, u.fl_final_costs.data(), 8 * nf);
+    if (from) std::memcpy(from, u.fl_from.data(), 4 * m);
+    if (to) std::memcpy(to, u.fl_to.data(), 4 * m);
+    if (ilabel) std::memcpy(ilabel, u.fl_il.data(), 4 * m);
+    if (olabel) std::memcpy(olabel, u.fl_ol.data(), 4 * m);
+    if (graph_cost) std::memcpy(graph_cost, u.fl_g.data(), 8 * m);
+    if (acoustic_cost) std::memcpy(acoustic_cost, u.fl_ac.data(), 8 * m);
+    return LB_OK;
+}
+
 int lb_result_counters(const lb_result *r, int32_t utt, int64_t *c) {
     UTT_OR_FAIL
     std::memcpy(c, u.counters, sizeof(u.counters));
@@ -894,6 +1129,53 @@ int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8
 }
 
 void lb_result_free(lb_result *r) { delete r; }
+
+int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const int64_t *final_ids,
+                        const double *final_costs, int64_t n_arcs, const int64_t *from, const int64_t *to,
+                        const int64_t *ilabel, const int64_t *olabel, const double *graph_cost,
+                        const double *acoustic_cost, char *buf, int64_t cap) {
+    std::string head = "NODES " + std::to_string(num_nodes) + " ARCS " + std::to_string(n_arcs) + " START " +
+                       std::to_string(start) + "\n";
+    for (int64_t i = 0; i < n_final; i++) {
+        head += "F " + std::to_string(final_ids[i]) + " ";
+        py_repr(final_costs[i], head);
+        head += "\n";
+    }
+    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n_arcs < 65536) nth = 1;
+    std::vector<std::string> part(nth);
+    auto work = [&](unsigned w) {
+        const int64_t lo = n_arcs * w / nth, hi = n_arcs * (w + 1) / nth;
+        std::string &o = part[w];
+        o.reserve((size_t)(hi - lo) * 48);
+        char ib[96];
+        for (int64_t k = lo; k < hi; k++) {
+            const int len = snprintf(ib, sizeof ib, "A %lld %lld %lld %lld ", (long long)from[k], (long long)to[k],
+                                     (long long)ilabel[k], (long long)olabel[k]);
+            o.append(ib, (size_t)len);
+            py_repr(graph_cost[k], o);
+            o += ' ';
+            py_repr(acoustic_cost[k], o);
+            o += '\n';
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nth; w++) th.emplace_back(work, w);
+    work(0);
+    for (auto &t : th) t.join();
+    int64_t total = (int64_t)head.size();
+    for (auto &p : part) total += (int64_t)p.size();
+    if (buf && cap >= total) {
+        char *q = buf;
+        std::memcpy(q, head.data(), head.size());
+        q += head.size();
+        for (auto &p : part) {
+            std::memcpy(q, p.data(), p.size());
+            q += p.size();
+        }
+    }
+    return total;
+}
 
 static int expand_common(lb_graph *g, const int32_t *states, const double *costs, int64_t n, const double *acrow,
                          int32_t D, double beam, double cutoff, int mode, int32_t *out_states, double *out_costs,

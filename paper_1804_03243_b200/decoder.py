@@ -44,8 +44,10 @@ class DecodeConfig:
     Added: `max_active` (0 = off, the reference behaviour; histogram cutoff,
     DESIGN.md §3), `token_arena` (tokens kept per utterance over all frames,
     0 = auto), `lanes` (utterances in flight per launch, 0 = auto),
-    `threads_per_lane` (CTA size, 0 = 1024), `ctas_per_lane` (thread-block
-    cluster size of a lane, 0 = auto), `device` (CUDA ordinal).
+    `threads_per_lane` (CTA size, 0 = 768), `ctas_per_lane` (thread-block
+    cluster size of a lane, 0 = auto), `device` (CUDA ordinal),
+    `keep_work_lattice` (also return `DecodeResult.work_lattice`, every live
+    arc with its extra cost; the final lattice is always built on the device).
     """
 
     beam: float = 14.0
@@ -64,6 +66,7 @@ class DecodeConfig:
     threads_per_lane: int = 0
     ctas_per_lane: int = 0
     device: int = 0
+    keep_work_lattice: bool = False
 
     def validate(self) -> None:
         if not (math.isfinite(self.beam) and self.beam > 0):
@@ -83,8 +86,8 @@ class DecodeConfig:
                      "device"):
             if int(getattr(self, name)) < 0:
                 raise UsageError(f"{name} must be >= 0")
-        if int(self.threads_per_lane) not in (0, 512, 640, 768):
-            raise UsageError("threads_per_lane must be 512, 640 or 768")
+        if int(self.threads_per_lane) not in (0, 512, 768):
+            raise UsageError("threads_per_lane must be 512 or 768")
         if not 0 <= int(self.ctas_per_lane) <= 4:
             raise UsageError("ctas_per_lane must be in [0, 4]")
 
@@ -93,7 +96,7 @@ class DecodeConfig:
                         int(self.max_active), int(self.max_tokens_per_frame),
                         int(self.max_lattice_arcs), int(self.token_arena), int(bool(want_lattice)),
                         int(bool(collect_frame_packs)), int(self.lanes), int(self.threads_per_lane),
-                        int(self.ctas_per_lane))
+                        int(self.ctas_per_lane), int(bool(self.keep_work_lattice)))
 
 
 @dataclass
@@ -283,10 +286,12 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
         alignment = list(zip(ils, range(len(ils))))
         r = DecodeResult(words, alignment, float(tc.value), bool(part.value), None, None, None,
                          None, counters)
-        if collect_frame_packs or want_lattice:
+        if want_lattice:
+            r.lattice = _final_lattice(res, u, m.shape[0])
+        if collect_frame_packs or (want_lattice and cfg.keep_work_lattice):
             try:
-                _attach_lattice(r, wfst, res, u, m, cfg, ntok.value, nlat.value, want_lattice,
-                                collect_frame_packs)
+                _attach_lattice(r, wfst, res, u, m, cfg, ntok.value, nlat.value,
+                                want_lattice and cfg.keep_work_lattice, collect_frame_packs)
             except Exception as exc:   # noqa: BLE001 - finalize failures are per utterance
                 out.append(exc)
                 continue
@@ -297,6 +302,25 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
                          "launches": tm["launches"], "total": time.perf_counter() - t0}
         out.append(r)
     return out
+
+
+def _final_lattice(res, u, num_frames) -> FinalLattice:
+    """The device-finalised lattice (lb_result_final_arrays) as a FinalLattice."""
+    L = _lib.lib()
+    nn, st, nf, na = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _raise_status(L.lb_result_final_lattice(res, u, C.byref(nn), C.byref(st), C.byref(nf), C.byref(na)),
+                  _lib.last_error())
+    keys = np.zeros(nn.value, dtype=np.uint64)
+    fids, fcs = np.zeros(nf.value, dtype=np.int64), np.zeros(nf.value)
+    fr, to, il, ol = (np.zeros(na.value, dtype=np.int32) for _ in range(4))
+    gc, ac = np.zeros(na.value), np.zeros(na.value)
+    _raise_status(L.lb_result_final_arrays(res, u, ptr(keys, PU64), ptr(fids, P64), ptr(fcs, PD),
+                                           ptr(fr, P32), ptr(to, P32), ptr(il, P32), ptr(ol, P32),
+                                           ptr(gc, PD), ptr(ac, PD)), _lib.last_error())
+    k = keys.astype(np.int64)
+    return FinalLattice(int(nn.value), int(st.value), fids, fcs, fr.astype(np.int64),
+                        to.astype(np.int64), il.astype(np.int64), ol.astype(np.int64), gc, ac,
+                        k >> 32, k & 0xFFFFFFFF, num_frames)
 
 
 def _attach_lattice(r, wfst, res, u, m, cfg, ntok, nlat, want_lattice, collect_frame_packs):
@@ -367,7 +391,6 @@ def _attach_lattice(r, wfst, res, u, m, cfg, ntok, nlat, want_lattice, collect_f
     lat = WorkLattice(wfst, frames, blocks, None, start_pos, r.partial,
                       None if r.partial else finals, r.total_cost)
     r.work_lattice = lat
-    r.lattice = finalize_lattice(lat)
 
 
 # ---------------------------------------------------------------------------

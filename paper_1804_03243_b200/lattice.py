@@ -205,6 +205,30 @@ def finalize_lattice(lat: WorkLattice) -> FinalLattice:
 
 
 def write_lattice_text(fl: FinalLattice) -> str:
+    """The reference lattice text (lattice.py:605-614), formatted by the native
+    library (multi-threaded, floats as Python repr; byte-identical to
+    `write_lattice_text_py`)."""
+    import ctypes as C
+
+    from . import _lib
+    L = _lib.host_lib()
+    i64 = [np.ascontiguousarray(getattr(fl, k), dtype=np.int64)
+           for k in ("final_ids", "from_", "to", "ilabel", "olabel")]
+    f64 = [np.ascontiguousarray(getattr(fl, k), dtype=np.float64)
+           for k in ("final_costs", "graph_cost", "acoustic_cost")]
+    P64, PD = _lib.P64, _lib.PD
+    args = (int(fl.num_nodes), int(fl.start), len(i64[0]), i64[0].ctypes.data_as(P64),
+            f64[0].ctypes.data_as(PD), len(i64[1]), i64[1].ctypes.data_as(P64),
+            i64[2].ctypes.data_as(P64), i64[3].ctypes.data_as(P64), i64[4].ctypes.data_as(P64),
+            f64[1].ctypes.data_as(PD), f64[2].ctypes.data_as(PD))
+    n = L.lb_lattice_text(*args, None, 0)
+    buf = C.create_string_buffer(int(n))
+    L.lb_lattice_text(*args, buf, n)
+    return buf.raw[:n].decode()
+
+
+def write_lattice_text_py(fl: FinalLattice) -> str:
+    """Pure-Python twin of write_lattice_text (the format's executable spec)."""
     out = [f"NODES {fl.num_nodes} ARCS {fl.num_arcs} START {fl.start}"]
     out += [f"F {fl.final_ids[i]} {float(fl.final_costs[i])!r}" for i in range(len(fl.final_ids))]
     out += [f"A {fl.from_[i]} {fl.to[i]} {fl.ilabel[i]} {fl.olabel[i]} "

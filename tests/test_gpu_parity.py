@@ -52,7 +52,7 @@ def test_larger_random_graphs(oracle_mod):
 def test_w1_and_diamond_kats():
     w1 = lb.load_wfst_text("0 1 1 1 0.5\n0 2 2 2 1.0\n1 0.0\n2 0.0\n")
     c1 = lb.load_cost_matrix("1 2\n0.3 0.1\n")
-    r = lb.decode_utterance(w1, c1)
+    r = lb.decode_utterance(w1, c1, lb.DecodeConfig(keep_work_lattice=True))
     assert r.words == [1] and r.alignment == [(1, 0)] and not r.partial
     assert r.total_cost == pytest.approx(0.8)
     assert r.lattice.num_arcs == 2
@@ -64,7 +64,7 @@ def test_w1_and_diamond_kats():
     dia = lb.load_wfst_text("0 1 1 1 0.1\n0 2 2 2 0.3\n1 3 1 0 0.2\n2 4 2 0 0.2\n"
                             "3 5 1 0 0.3\n4 5 2 0 0.3\n5 0.0\n")
     dc = lb.load_cost_matrix("3 2\n0.1 0.2\n0.1 0.2\n0.2 0.2\n")
-    r = lb.decode_utterance(dia, dc, lb.DecodeConfig(lattice_beam=8.0))
+    r = lb.decode_utterance(dia, dc, lb.DecodeConfig(lattice_beam=8.0, keep_work_lattice=True))
     assert r.total_cost == pytest.approx(1.0)
     by = {}
     for a in r.work_lattice.arcs():

@@ -82,6 +82,24 @@ class TestFormats:
             with pytest.raises(lb.ParseError):
                 lb.read_lattice_text(bad)
 
+    def test_native_text_writer_matches_python_repr(self):
+        """lb_lattice_text (native, threaded) == the pure-Python writer, byte for byte,
+        over awkward floats (repr switches to exponent form at 1e-4 / 1e16, keeps
+        '.0' on integral values, shortest round-trip digits) and a big lattice."""
+        from paper_1804_03243_b200.lattice import write_lattice_text_py
+        vals = np.array([0.0, -0.0, 1.0, 100.0, 0.1, 1 / 3, 1e-4, 1e-5, 9.999e-5, 1e15, 1e16, 123456.789,
+                         2.5e-300, 1.7976931348623157e308, 5e-324, 0.30000000000000004, 7.0e22, -3.25])
+        n = len(vals)
+        fl = lb.FinalLattice(n + 1, 0, np.array([n]), np.array([vals[3]]), np.arange(n), np.arange(1, n + 1),
+                             np.arange(n) % 7, np.arange(n) % 5, vals, vals[::-1].copy())
+        assert lb.write_lattice_text(fl) == write_lattice_text_py(fl)
+        rng = np.random.default_rng(3)
+        m = 200_000
+        big = lb.FinalLattice(m + 1, 0, np.array([m, m - 1]), rng.uniform(0, 3, 2), np.arange(m),
+                              np.arange(1, m + 1), rng.integers(0, 3000, m), rng.integers(0, 30000, m),
+                              rng.uniform(0, 3, m), rng.uniform(-5, 5, m) * 10.0 ** rng.integers(-8, 8, m))
+        assert lb.write_lattice_text(big) == write_lattice_text_py(big)
+
     def test_npz_roundtrip(self, tmp_path):
         w = synthetic.hclg_graph(1, num_states=5000, pool_size=200)
         p = tmp_path / "g.npz"
