@@ -349,7 +349,7 @@ struct Lane {
         if (threadIdx.x == 0) lane_sm.nfr[0] = lane_sm.nfr[1] = lane_sm.nfr[2] = 0;
         const unsigned long long t0 = wbegin();
         auto fill_tail = [&]() {
-            for (int i = cused + lane; i < CCH; i += 32) __stcg(cb + cstart + i, make_int4(-1, 0, 0, 0));
+            for (int i = cused + lane; i < CCH; i += 32) __stcs(cb + cstart + i, make_int4(-1, 0, 0, 0));
         };
         for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan, wmap(),
                                         [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
@@ -417,9 +417,9 @@ struct Lane {
                         const long long bits = __double_as_longlong(cand[u]);
                         const unsigned flag = (unsigned)r[u].y & EPS_FLAG;
                         const int k = cstart + cused + off[u];
-                        __stcg(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
+                        __stcs(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
                                                  (int)(bits & 0xFFFFFFFFll), (int)(bits >> 32)));
-                        __stcg(cbi + k, ii[u]);
+                        __stcs(cbi + k, ii[u]);
                     }
                 }
             }
@@ -514,8 +514,8 @@ struct Lane {
                 const int k = kb + u * 32 + lane;
                 e[u].x = -1;
                 if (k < nc) {
-                    e[u] = __ldcg(cb + k);
-                    if (e[u].x != -1) ti[u] = __ldcg(cbi + k);
+                    e[u] = __ldcs(cb + k);
+                    if (e[u].x != -1) ti[u] = __ldcs(cbi + k);
                 }
             }
             unsigned long long pk[WUNR];
@@ -767,10 +767,10 @@ struct Lane {
                 const long long o = tb + idx;
                 __stcg(io.tok_state + o, v);
                 __stcg(io.tok_cost + o, init ? 0.0 : c);
-                __stcg(io.tok_arc + o, init ? -1 : (int)st.arc[i]);
-                __stcg(io.tok_pred + o, init ? -1 : pr);
+                __stcs(io.tok_arc + o, init ? -1 : (int)st.arc[i]);
+                __stcs(io.tok_pred + o, init ? -1 : pr);
                 if (p.collect_packs)
-                    __stcg(io.tok_pack + o, ((unsigned long long)st.key[i] << 32) | st.arc[i]);
+                    __stcs(io.tok_pack + o, ((unsigned long long)st.key[i] << 32) | st.arc[i]);
                 store_rec32(&rec[v], c, pr, idx, SENT, st.msnap[i]);
                 fx = !init && (pr & 1) == 0;
             } else if (i < st.n) {
