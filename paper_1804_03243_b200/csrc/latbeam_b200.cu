@@ -19,6 +19,7 @@
 #include "../../include/latbeam_b200.h"
 #include "lb_kernels.cuh"
 #include "lb_lattice.cuh"
+#include "lb_batched.cuh"
 
 using namespace lbk;
 
@@ -108,6 +109,7 @@ struct Workspace {
     double *out_d = nullptr;
     LaneWs *d_lanes = nullptr;
     UttDesc *d_desc = nullptr;
+    LaneCtl *d_ctl = nullptr;   // batched mode: per-lane control blocks
     std::vector<void *> owned;
 
     void release() {
@@ -226,6 +228,7 @@ int ensure_workspace(lb_graph *g, int lanes, int C, int64_t ccap, int64_t tok_ca
     CK(A(&w.out_c, 8 * nl));
     CK(A(&w.d_lanes, nl));
     CK(A(&w.d_desc, nl));
+    CK(A(&w.d_ctl, nl));
     init_rec<<<g->sms * 4, 256, 0, g->stream>>>(w.rec, (long long)(S * nl));
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(w.rpk, 0xFF, 2 * S * nl * sizeof(EpsWin), g->stream));
@@ -516,6 +519,90 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
     return LB_OK;
 }
 
+// One wave in the frame-synchronous batched mode (lb_batched.cuh): 6-7 phase
+// kernels per frame over all nw lanes, launched back to back on the stream.
+int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T, int bpl,
+                   cudaStream_t st, lb_result *res) {
+    int tmax = 0;
+    for (int l = 0; l < nw; l++) tmax = std::max(tmax, (int)T[l]);
+    const LaneWs *lw = w.d_lanes;
+    const UttDesc *ud = w.d_desc;
+    LaneCtl *ctl = w.d_ctl;
+    const dim3 grid((unsigned)bpl, (unsigned)nw);
+    constexpr int ENT = 512, ECL = 2, FNT = 512;
+    cudaLaunchConfig_t ec = {};
+    ec.gridDim = dim3((unsigned)(nw * ECL));
+    ec.blockDim = dim3(ENT);
+    ec.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ECL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    ec.attrs = at;
+    ec.numAttrs = 1;
+    int launches = 0;
+    // LB_BATCH_PROFILE=1: CUDA-event time per phase kernel, summed (stderr)
+    const bool bprof = getenv("LB_BATCH_PROFILE") != nullptr;
+    std::vector<cudaEvent_t> evs;
+    std::vector<int> ev_kind;
+    auto mark = [&](int kind) {
+        if (!bprof) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        evs.push_back(e);
+        ev_kind.push_back(kind);
+    };
+    auto eps = [&]() -> int {
+        if (!gd.has_eps) return LB_OK;
+        CK(cudaLaunchKernelEx(&ec, b_epsilon<ENT>, gd, p, lw, (LaneCtl *)ctl, nw));
+        launches++;
+        return LB_OK;
+    };
+    mark(-1);
+    b_init<<<nw, 32, 0, st>>>(gd, p, lw, ud, ctl, nw);
+    if (int rc = eps()) return rc;
+    b_aggregate<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+    b_turnover<<<nw, 32, 0, st>>>(p, ud, ctl, nw);
+    mark(6);
+    launches += 3;
+    for (int t = 1; t <= tmax; t++) {
+        b_emit<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+        mark(0);
+        b_winners<<<grid, BNT, 0, st>>>(gd, p, lw, ctl, nw);
+        mark(1);
+        b_max_active<<<nw, 32, 0, st>>>(p, ctl, nw);
+        mark(2);
+        if (int rc = eps()) return rc;
+        mark(3);
+        b_aggregate<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+        mark(4);
+        b_turnover<<<nw, 32, 0, st>>>(p, ud, ctl, nw);
+        mark(5);
+        launches += 5;
+    }
+    if (bprof) {
+        cudaStreamSynchronize(st);
+        double acc[8] = {0};
+        for (size_t k = 1; k < evs.size(); k++) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, evs[k - 1], evs[k]);
+            acc[ev_kind[k]] += ms;
+        }
+        const char *nm[7] = {"emit", "winners", "max_active", "epsilon", "aggregate", "turnover", "frame0"};
+        fprintf(stderr, "[batched profile] frames=%d lanes=%d bpl=%d  ", tmax, nw, bpl);
+        for (int k = 0; k < 7; k++) fprintf(stderr, "%s=%.1fus ", nm[k], acc[k] * 1e3 / std::max(tmax, 1));
+        fprintf(stderr, "(per frame)\n");
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    b_final<FNT><<<nw, FNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+    launches++;
+    CK(cudaGetLastError());
+    res->launches += launches;
+    return LB_OK;
+}
+
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms) {
     const bool lat = cfg->want_lattice != 0;
@@ -531,12 +618,26 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
-    const int C = cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2;
+    // Mode: the frame-synchronous batched kernels (lb_batched.cuh) spread every
+    // phase over all SMs and win for small batches (1 utterance: 13k vs 8k
+    // frames/s); the persistent-lane kernel overlaps the lanes' phases and wins
+    // from ~40 concurrent utterances up (64: 389k vs 312k frames/s, measured on
+    // C2/C4).  Lattice decodes use the lane kernel.  LB_MODE=lane|batched overrides.
+    const char *mode_env = getenv("LB_MODE");
+    bool batched = !lat && n <= BATCHED_MAX_UTTS;
+    if (mode_env && !strcmp(mode_env, "lane")) batched = false;
+    if (mode_env && !strcmp(mode_env, "batched") && !lat) batched = true;
+    const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2);
     const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
-    const int64_t ccap = cand_capacity(g, max_tok, C, threads);
+    int lanes_guess = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / 2));
+    lanes_guess = std::max(1, std::min(lanes_guess, n > 0 ? n : 1));
+    const int bpl = std::max(1, (g->sms * 4) / lanes_guess);   // batched: blocks per lane per phase kernel
+    const int64_t ccap = batched ? std::min<int64_t>(g->A_emit, max_tok * g->max_edeg) +
+                                       (int64_t)(bpl * BNW + 1) * BCCH
+                                 : cand_capacity(g, max_tok, C, threads);
     // lanes: requested, else as many as fit a memory budget (<= 1 wave of SMs)
     const size_t per_lane = lane_bytes(S, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
-    int lanes = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / C));
+    int lanes = batched ? lanes_guess : (cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / C)));
     lanes = std::max(1, std::min(lanes, n > 0 ? n : 1));
     const Workspace &w0 = g->ws;
     const bool fits = w0.lanes >= lanes && w0.C == C && w0.S == g->S && w0.ccap >= ccap && w0.tok_cap >= tok_cap &&
@@ -611,7 +712,10 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaMemcpyAsync(w.d_desc, desc.data(), nw * sizeof(UttDesc), cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(w.out_i, 0, 8 * sizeof(int) * nw, st));
         CK(cudaEventRecord(e0, st));
-        {
+        if (batched) {
+            int rcb = launch_batched(g, gd, p, w, nw, T + w0, bpl, st, res);
+            if (rcb) return rcb;
+        } else {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)(nw * C));
             lc.blockDim = dim3((unsigned)threads);
@@ -625,8 +729,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             lc.attrs = at;
             lc.numAttrs = 1;
             CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc, nw));
+            res->launches++;
         }
-        res->launches++;
         CK(cudaEventRecord(e1, st));
         if (lat) {
             prune_kernel<<<nw, threads, 0, st>>>(gd, p, w.d_desc, nw);
@@ -951,7 +1055,13 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     // 1-best decodes read each frame's row once per lane: the kernel reads the
     // mapped staging buffer directly (zero-copy, overlapped with decoding).
     // Lattice decodes re-read rows in the prune pass: copy them to HBM.
-    const bool zero_copy = !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX && !getenv("LB_E2E_COPY");
+    // (only the persistent-lane kernel reads rows once per frame; the batched mode
+    // gathers acoustic costs per candidate and needs them in HBM)
+    const char *mode_env = getenv("LB_MODE");
+    const bool lane_mode = cfg->want_lattice || (mode_env && !strcmp(mode_env, "lane")) ||
+                           (n > BATCHED_MAX_UTTS && !(mode_env && !strcmp(mode_env, "batched")));
+    const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
+                           !getenv("LB_E2E_COPY");
     std::vector<const double *> dptr(n);
     float h2d = stage_ms;
     if (zero_copy) {

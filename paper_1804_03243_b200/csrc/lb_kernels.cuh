@@ -135,12 +135,12 @@ __device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
 // full-mask warp collectives.
 constexpr int WMAP = 512;
 template <int UNR, class F>
-__device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, const Grp &G,
+__device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, int gwarp, int gnw,
                                                            const unsigned *ts, const double *tc, int n,
                                                            unsigned &c_scan, int *own, F &&f) {
     const int lane = threadIdx.x & 31;
-    const int step = G.gnw() * 32;
-    int base = G.gwarp() * 32;
+    const int step = gnw * 32;
+    int base = gwarp * 32;
     unsigned s = 0u;
     double c = 0.0;
     if (base + lane < n) {
@@ -351,7 +351,7 @@ struct Lane {
         auto fill_tail = [&]() {
             for (int i = cused + lane; i < CCH; i += 32) __stcs(cb + cstart + i, make_int4(-1, 0, 0, 0));
         };
-        for_each_token_arc_batched<UNR>(g, G, pts, ptc, np, c_scan, wmap(),
+        for_each_token_arc_batched<UNR>(g, G.gwarp(), G.gnw(), pts, ptc, np, c_scan, wmap(),
                                         [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
             int4 r[UNR];
 #pragma unroll
@@ -860,7 +860,7 @@ struct Lane {
                            long long lb) {
         if (frame > 0) {
             unsigned dummy = 0;
-            for_each_token_arc_batched<UNR>(g, G, io.tok_state + tbp, io.tok_cost + tbp, np, dummy, wmap(),
+            for_each_token_arc_batched<UNR>(g, G.gwarp(), G.gnw(), io.tok_state + tbp, io.tok_cost + tbp, np, dummy, wmap(),
                                             [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
 #pragma unroll
                 for (int u = 0; u < UNR; u++) {

@@ -41,6 +41,37 @@ def test_random_corpus(oracle_mod, base, cycles, negative):
     assert kinds.get("exact", 0) >= 20, kinds
 
 
+@pytest.mark.parametrize("mode", ["batched", "lane"])
+@pytest.mark.parametrize("base,cycles,negative", [(11_000_000, True, False), (12_000_000, False, True)])
+def test_random_corpus_1best_modes(oracle_mod, monkeypatch, mode, base, cycles, negative):
+    """1-best decodes (per-frame packs bit-exact) through both device modes: the
+    frame-synchronous batched kernels and the persistent-lane kernel."""
+    monkeypatch.setenv("LB_MODE", mode)
+    rng = np.random.default_rng(base)
+    for seed in range(base, base + 40):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=cycles, allow_negative=negative)
+        beam = float(rng.uniform(3.0, 14.0))
+        scale = 1.0 if seed % 3 else 0.75
+        got, ref = decode_both(w, m, oracle_mod, beam, 4.0, scale, want_lattice=False,
+                               max_active=int(rng.integers(0, 12)))
+        check_pair(got, ref, 4.0, want_lattice=False)
+
+
+def test_c4_batched_mode_matches_lane_mode(oracle_mod, monkeypatch):
+    """The 64-utterance C4 batch in both modes: identical costs and paths."""
+    w = synthetic.hclg_graph(2, num_states=400_000, pool_size=6000, num_pdfs=600)
+    mats = [synthetic.hclg_matrix(500 + i, num_frames=40, num_pdfs=600) for i in range(64)]
+    cfg = lb.DecodeConfig(beam=13.0, max_active=2500)
+    out = {}
+    for mode in ("batched", "lane"):
+        monkeypatch.setenv("LB_MODE", mode)
+        out[mode] = lb.decode_batch(w, mats, cfg, want_lattice=False)
+    assert [r.total_cost for r in out["batched"]] == [r.total_cost for r in out["lane"]]
+    assert [r.words for r in out["batched"]] == [r.words for r in out["lane"]]
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 13.0, max_active=2500)
+    assert [r.total_cost for r in out["batched"]] == tc.tolist()
+
+
 def test_larger_random_graphs(oracle_mod):
     for seed in range(9_000_000, 9_000_012):
         w, m = synthetic.random_task(seed, max_states=400, max_arcs=3000, num_labels=30,
@@ -216,6 +247,8 @@ def test_compute_sanitizer_clean(tool):
         "w = synthetic.hclg_graph(5, num_states=20000, pool_size=500, num_pdfs=100)\n"
         "ms = [synthetic.hclg_matrix(9 + i, num_frames=6, num_pdfs=100) for i in range(2)]\n"
         "r = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, lattice_beam=3.0, max_active=300))\n"
+        "q = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300), want_lattice=False)\n"
+        "assert [x.total_cost for x in r] == [x.total_cost for x in q]\n"
         "print('ok', [x.total_cost for x in r])\n" % root)
     res = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable, "-c", prog],
                          capture_output=True, text=True, timeout=1200)
