@@ -564,6 +564,7 @@ int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &
     b_init<<<nw, 32, 0, st>>>(gd, p, lw, ud, ctl, nw);
     if (int rc = eps()) return rc;
     b_aggregate<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+    if (p.want_lattice) b_lattice<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
     b_turnover<<<nw, 32, 0, st>>>(p, ud, ctl, nw);
     mark(6);
     launches += 3;
@@ -577,6 +578,7 @@ int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &
         if (int rc = eps()) return rc;
         mark(3);
         b_aggregate<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
+        if (p.want_lattice) b_lattice<<<grid, BNT, 0, st>>>(gd, p, lw, ud, ctl, nw);
         mark(4);
         b_turnover<<<nw, 32, 0, st>>>(p, ud, ctl, nw);
         mark(5);
@@ -624,9 +626,9 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     // from ~40 concurrent utterances up (64: 389k vs 312k frames/s, measured on
     // C2/C4).  Lattice decodes use the lane kernel.  LB_MODE=lane|batched overrides.
     const char *mode_env = getenv("LB_MODE");
-    bool batched = !lat && n <= BATCHED_MAX_UTTS;
+    bool batched = n <= BATCHED_MAX_UTTS;
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;
-    if (mode_env && !strcmp(mode_env, "batched") && !lat) batched = true;
+    if (mode_env && !strcmp(mode_env, "batched")) batched = true;
     const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2);
     const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
     int lanes_guess = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / 2));

@@ -560,6 +560,74 @@ __global__ void __launch_bounds__(BNT, 4) b_aggregate(const __grid_constant__ Gr
 }
 
 // ---------------------------------------------------------------------------
+// lattice arcs of block t (rule A.5, lattice.py:313-362): emitting arc live iff
+// its candidate <= cutoff and its destination was kept; epsilon arc live iff both
+// ends kept and min-snapshot(src) + w <= cutoff.  Resets minsnap.
+__device__ __forceinline__ bool b_kept(const LaneWs &L, const UttDesc &io, unsigned v, long long tb, int n, int &j) {
+    j = __ldcg(&L.rec[v].tokidx);
+    return j >= 0 && j < n && __ldcg(io.tok_state + tb + j) == v;
+}
+
+__global__ void __launch_bounds__(BNT, 4) b_lattice(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
+                                                    const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts,
+                                                    LaneCtl *__restrict__ ctl, int n_lanes) {
+    __shared__ int own_s[BNW][WMAP];
+    const int l = blockIdx.y;
+    if (l >= n_lanes) return;
+    LaneCtl &c = ctl[l];
+    if (!c.active) return;
+    const LaneWs &L = lanes[l];
+    const UttDesc &io = utts[l];
+    const int t = c.t;
+    const int warp = threadIdx.x >> 5;
+    const double cutoff = c.cutoff;
+    const long long tb = c.tb, lb = c.lb;
+    const int n = c.ntok_new;
+    auto push = [&](int arc, int from, int to) {
+        const int sl = agg_append(&c.nlat);
+        const long long gs = lb + sl;
+        if (gs < io.lat_cap) {
+            __stcg(io.lat_arc + gs, arc);
+            __stcg(io.lat_from + gs, from);
+            __stcg(io.lat_to + gs, to);
+        }
+    };
+    if (t > 0) {
+        const double *row = io.costs + (long long)(t - 1) * p.D;
+        unsigned dummy = 0;
+        for_each_token_arc_batched<BUNR>(g, blockIdx.x * BNW + warp, gridDim.x * BNW, io.tok_state + c.tbp,
+                                         io.tok_cost + c.tbp, c.ntok, dummy, own_s[warp],
+                                         [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
+#pragma unroll
+            for (int u = 0; u < BUNR; u++) {
+                if (!vv[u]) continue;
+                const int4 r = __ldg(g.arcs + aa[u]);
+                const unsigned il = arc_il(r.y);
+                if (il == 0) continue;
+                const double cand = __dadd_rn(__dadd_rn(cc[u], __hiloint2double(r.w, r.z)), b_ac(row, il, p.scale));
+                int j;
+                if (cand <= cutoff && b_kept(L, io, (unsigned)r.x, tb, n, j)) push((int)aa[u], ii[u], j);
+            }
+        });
+    }
+    if (g.has_eps) {
+        const double inf = inf_d();
+        for (int j = blockIdx.x * BNT + threadIdx.x; j < n; j += gridDim.x * BNT) {
+            const unsigned u = __ldcg(io.tok_state + tb + j);
+            const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
+            const double ms = __ldcg(&L.rec[u].minsnap);
+            __stcg(&L.rec[u].minsnap, inf);
+            for (unsigned e = e0; e < e1; ++e) {
+                const int4 r = __ldg(g.eps + e);
+                int jv;
+                if (__dadd_rn(ms, __hiloint2double(r.w, r.z)) <= cutoff && b_kept(L, io, (unsigned)r.x, tb, n, jv))
+                    push(r.y, j, jv);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // turnover: close frame t (checks, offsets, counters), open frame t+1.
 __global__ void __launch_bounds__(32) b_turnover(const Params p, const UttDesc *utts, LaneCtl *ctl, int n) {
     const int l = blockIdx.x;
@@ -578,7 +646,17 @@ __global__ void __launch_bounds__(32) b_turnover(const Params p, const UttDesc *
         return;
     }
     io.tok_base[t + 1] = c.tb + k;
-    if (p.want_lattice) io.lat_base[t + 1] = c.lb;
+    if (p.want_lattice) {
+        const long long lb = c.lb + c.nlat;
+        if (lb > io.lat_cap) {
+            ctl_error(c, E_CAP_LATTICE, t, lb);
+            c.dirty = 0;
+            return;
+        }
+        c.lb = lb;
+        c.nlat = 0;
+        io.lat_base[t + 1] = lb;
+    }
     if (t > 0) c.c[6] += (unsigned long long)k;
     c.tbp = c.tb;
     c.tb += k;

@@ -25,9 +25,12 @@ def test_native_library_is_the_path():
     assert L.lb_version() == 1
 
 
+@pytest.mark.parametrize("mode", ["batched", "lane"])
 @pytest.mark.parametrize("base,cycles,negative", [(0, False, False), (1_000_000, False, True),
                                                   (7_000_000, True, False), (3_000_000, True, True)])
-def test_random_corpus(oracle_mod, base, cycles, negative):
+def test_random_corpus(oracle_mod, monkeypatch, mode, base, cycles, negative):
+    """1-best + lattice on random graphs, through both device modes."""
+    monkeypatch.setenv("LB_MODE", mode)
     rng = np.random.default_rng(base + 17)
     kinds = {}
     for seed in range(base, base + 60):
