@@ -146,6 +146,11 @@ struct lb_graph {
     cudaStream_t stream = nullptr;
     std::mutex mu;
     Workspace ws;
+    // batched mode: captured CUDA graph of one wave's launch sequence, reused
+    // while (workspace, lanes, frames, blocks per lane, Params) stay the same
+    cudaGraphExec_t bexec = nullptr;
+    std::string bkey;
+    int blaunches = 0;
     double *d_costs = nullptr;
     size_t d_costs_cap = 0;
     double *h_stage = nullptr;
@@ -521,8 +526,49 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
 
 // One wave in the frame-synchronous batched mode (lb_batched.cuh): 6-7 phase
 // kernels per frame over all nw lanes, launched back to back on the stream.
+int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T,
+                       int bpl, cudaStream_t st, lb_result *res);
+
+// The per-frame launch sequence is captured once into a CUDA graph and replayed:
+// ~7 launches per frame would otherwise cost more CPU time than a small batch's
+// GPU time, and the graph also shortens the GPU-side gaps between the kernels.
 int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T, int bpl,
                    cudaStream_t st, lb_result *res) {
+    if (getenv("LB_BATCH_PROFILE") || getenv("LB_NO_GRAPH")) return launch_batched_seq(g, gd, p, w, nw, T, bpl, st, res);
+    int tmax = 0;
+    for (int l = 0; l < nw; l++) tmax = std::max(tmax, (int)T[l]);
+    std::string key((const char *)&p, sizeof(Params));
+    key += std::to_string(nw) + "/" + std::to_string(tmax) + "/" + std::to_string(bpl) + "/" +
+           std::to_string((unsigned long long)(uintptr_t)w.d_lanes) + "/" +
+           std::to_string((unsigned long long)(uintptr_t)w.d_ctl) + "/" +
+           std::to_string((unsigned long long)(uintptr_t)w.d_desc);
+    if (!g->bexec || g->bkey != key) {
+        if (g->bexec) {
+            cudaGraphExecDestroy(g->bexec);
+            g->bexec = nullptr;
+        }
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        lb_result dummy;
+        const int rc = launch_batched_seq(g, gd, p, w, nw, T, bpl, cs, &dummy);
+        cudaGraph_t graph;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return set_err(LB_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        CK(cudaGraphInstantiate(&g->bexec, graph, 0));
+        cudaGraphDestroy(graph);
+        g->bkey = key;
+        g->blaunches = dummy.launches;
+    }
+    CK(cudaGraphLaunch(g->bexec, st));
+    res->launches += g->blaunches;
+    return LB_OK;
+}
+
+int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T,
+                       int bpl, cudaStream_t st, lb_result *res) {
     int tmax = 0;
     for (int l = 0; l < nw; l++) tmax = std::max(tmax, (int)T[l]);
     const LaneWs *lw = w.d_lanes;
@@ -620,11 +666,12 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
-    // Mode: the frame-synchronous batched kernels (lb_batched.cuh) spread every
-    // phase over all SMs and win for small batches (1 utterance: 13k vs 8k
-    // frames/s); the persistent-lane kernel overlaps the lanes' phases and wins
-    // from ~40 concurrent utterances up (64: 389k vs 312k frames/s, measured on
-    // C2/C4).  Lattice decodes use the lane kernel.  LB_MODE=lane|batched overrides.
+    // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
+    // CUDA graph) spread every phase over all SMs and win for small batches
+    // (1 utterance: 17.8k vs 8.1k frames/s; 32: 264k vs 225k); the
+    // persistent-lane kernel overlaps the lanes' phases and wins from ~48
+    // concurrent utterances up (64: 388k vs 333k frames/s; C2 graph, measured).
+    // LB_MODE=lane|batched overrides.
     const char *mode_env = getenv("LB_MODE");
     bool batched = n <= BATCHED_MAX_UTTS;
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;
@@ -980,6 +1027,7 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
 int lb_graph_destroy(lb_graph *g) {
     if (!g) return LB_OK;
     cudaSetDevice(g->device);
+    if (g->bexec) cudaGraphExecDestroy(g->bexec);
     g->ws.release();
     cudaFree(g->arcs);
     cudaFree(g->src);
