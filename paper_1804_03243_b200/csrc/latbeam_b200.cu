@@ -151,6 +151,7 @@ struct lb_graph {
     cudaGraphExec_t bexec = nullptr;
     std::string bkey;
     int blaunches = 0;
+    FlScratch fl;   // lattice finaliser scratch, grown on demand and reused
     double *d_costs = nullptr;
     size_t d_costs_cap = 0;
     double *h_stage = nullptr;
@@ -749,7 +750,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     CK(cudaEventCreate(&e3));
     res->utts.resize(n);
     res->t_h2d = h2d_ms;
-    FlScratch fl;
+    FlScratch &fl = g->fl;
     std::vector<UttDesc> desc(lanes);
     std::vector<int> hi(8 * lanes);
     std::vector<double> hd(4 * lanes);
@@ -782,8 +783,20 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         }
         CK(cudaEventRecord(e1, st));
         if (lat) {
-            prune_kernel<<<nw, threads, 0, st>>>(gd, p, w.d_desc, nw);
-            CK(cudaGetLastError());
+            // one cluster per utterance, as wide as the GPU allows (portable max 8)
+            const unsigned pc = (unsigned)std::max(1, std::min(8, g->sms / std::max(nw, 1)));
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)nw * pc);
+            lc.blockDim = dim3(1024);
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = pc;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&lc, prune_kernel, gd, p, (const UttDesc *)w.d_desc, nw));
             res->launches++;
         }
         CK(cudaEventRecord(e2, st));

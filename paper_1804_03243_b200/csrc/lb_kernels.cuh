@@ -1178,19 +1178,36 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     G.sync();   // keep rank 0's shared memory alive until every CTA is done with it
 }
 
+// largest b with base[b] <= k (base has nb non-decreasing entries)
+__device__ __forceinline__ int upper_block(const long long *base, int nb, long long k) {
+    int lo = 0, hi = nb - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (base[mid] <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 // ===========================================================================
-// Lattice extra-cost pruning (lattice.py:365-497) from the final terminus,
-// one CTA per utterance: backward over frames, emitting arcs relax node
-// extras with a 64-bit atomicMin on the order-preserving f64 encoding, the
-// in-frame epsilon fixpoint runs Jacobi iterations, then every arc is flagged.
+// Lattice extra-cost pruning (lattice.py:365-497) from the final terminus, one
+// thread-block cluster per utterance (cluster size chosen by the host so the
+// whole GPU works even for one utterance): backward over frames, emitting arcs
+// relax node extras with a 64-bit atomicMin on the order-preserving f64
+// encoding, the in-frame epsilon fixpoint runs Jacobi iterations, then every
+// arc is flagged.  Phases of a frame meet at cluster barriers.
 // ===========================================================================
 __global__ void __launch_bounds__(1024, 1)
 prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts) {
     __shared__ int s_moved;
-    if ((int)blockIdx.x >= n_utts) return;
-    const UttDesc io = utts[blockIdx.x];
-    if (io.out_i[0] != E_OK) return;
-    const int tid = threadIdx.x, bd = blockDim.x;
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int u = blockIdx.x / C;
+    if (u >= n_utts) return;
+    const UttDesc io = utts[u];
+    if (io.out_i[0] != E_OK) return;   // uniform across the cluster
+    int *m0 = cl.map_shared_rank(&s_moved, 0);
+    const int tid = rank * blockDim.x + threadIdx.x, bd = C * blockDim.x;
     const int T = io.T;
     const bool partial = io.out_i[2] != 0;
     const double best_total = io.out_d[1];
@@ -1207,10 +1224,10 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
                 const double x = partial ? 0.0 : __dsub_rn(__dadd_rn(__ldcg(fwd + i), __ldg(g.fin + s)), best_total);
                 __stcg(ne + i, enc64(x));
             }
-            __syncthreads();
+            cl.sync();
         } else {
             for (int i = tid; i < nfr; i += bd) __stcg(ne + i, enc64(inf));
-            __syncthreads();
+            cl.sync();
             const long long b1 = io.tok_base[f + 1];
             const double *fwdn = io.tok_cost + b1;
             const double *nen = io.node_extra + b1;
@@ -1225,16 +1242,16 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
                 const double acv = __dmul_rn(__ldg(row + il - 1), p.scale);
                 const double c = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(__ldcg(fwd + from), w), acv), __ldcg(fwdn + to)),
                                            __ldcg(nen + to));
-                atomicMin(ne + from, enc64(c));
+                atom_min_u64(ne + from, enc64(c));
             }
-            __syncthreads();
+            cl.sync();
         }
         // in-frame epsilon fixpoint (lattice.py:455-469)
         if (g.has_eps) {
             const long long k0 = io.lat_base[f], k1 = io.lat_base[f + 1];
             for (int it = 0;; it++) {
-                if (tid == 0) s_moved = 0;
-                __syncthreads();
+                if (rank == 0 && threadIdx.x == 0) s_moved = 0;
+                cl.sync();
                 for (long long k = k0 + tid; k < k1; k += bd) {
                     const unsigned a = (unsigned)__ldcg(io.lat_arc + k);
                     unsigned dst, il;
@@ -1245,18 +1262,18 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
                     const double base = __dsub_rn(__dadd_rn(__ldcg(fwd + from), w), __ldcg(fwd + to));
                     const double c = __dadd_rn(base, dec64(__ldcg(ne + to)));
                     const double before = dec64(__ldcg(ne + from));
-                    io.tmp[k] = c;
-                    if (__dsub_rn(before, c) > CONVERGE_TOL) s_moved = 1;
+                    __stcg(io.tmp + k, c);
+                    if (__dsub_rn(before, c) > CONVERGE_TOL) *m0 = 1;
                 }
-                __syncthreads();
+                cl.sync();
                 for (long long k = k0 + tid; k < k1; k += bd) {
                     const unsigned a = (unsigned)__ldcg(io.lat_arc + k);
                     if (arc_il(__ldg(g.arcs + a).y) != 0) continue;
-                    atomicMin(ne + __ldcg(io.lat_from + k), enc64(io.tmp[k]));
+                    atom_min_u64(ne + __ldcg(io.lat_from + k), enc64(__ldcg(io.tmp + k)));
                 }
-                __syncthreads();
-                const int moved = s_moved;
-                __syncthreads();
+                cl.sync();
+                const int moved = *m0;
+                cl.sync();
                 if (!moved) break;
                 if (it >= nfr) {
                     if (tid == 0) io.out_i[0] = E_INT_PRUNE_EPS, io.out_i[1] = f;
@@ -1268,24 +1285,24 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
             const double x = dec64(__ldcg(ne + i));
             __stcg(io.node_extra + b0 + i, x < 0.0 ? 0.0 : x);
         }
-        __syncthreads();
+        cl.sync();
     }
-    // flag pass (lattice.py:473-497)
-    for (int b = 0; b <= T; b++) {
+    // flag pass (lattice.py:473-497): every arc's extra, all blocks at once
+    const long long nl = io.lat_base[T + 1];
+    for (long long k = tid; k < nl; k += bd) {
+        const int b = upper_block(io.lat_base, T + 2, k);
         const long long tbb = io.tok_base[b];
-        for (long long k = io.lat_base[b] + tid; k < io.lat_base[b + 1]; k += bd) {
-            const unsigned a = (unsigned)__ldcg(io.lat_arc + k);
-            unsigned dst, il;
-            double w;
-            load_arc(g.arcs, a, dst, il, w);
-            const int from = __ldcg(io.lat_from + k), to = __ldcg(io.lat_to + k);
-            const long long fb = il > 0 ? io.tok_base[b - 1] : tbb;
-            const double acv = il > 0 ? __dmul_rn(__ldg(io.costs + (long long)(b - 1) * D + il - 1), p.scale) : 0.0;
-            const double x = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(__ldcg(io.tok_cost + fb + from), w), acv),
-                                                 __ldcg(io.tok_cost + tbb + to)),
-                                       __ldcg(io.node_extra + tbb + to));
-            io.lat_extra[k] = x < 0.0 ? 0.0 : x;
-        }
+        const unsigned a = (unsigned)__ldcg(io.lat_arc + k);
+        unsigned dst, il;
+        double w;
+        load_arc(g.arcs, a, dst, il, w);
+        const int from = __ldcg(io.lat_from + k), to = __ldcg(io.lat_to + k);
+        const long long fb = il > 0 ? io.tok_base[b - 1] : tbb;
+        const double acv = il > 0 ? __dmul_rn(__ldg(io.costs + (long long)(b - 1) * D + il - 1), p.scale) : 0.0;
+        const double x = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(__ldcg(io.tok_cost + fb + from), w), acv),
+                                             __ldcg(io.tok_cost + tbb + to)),
+                                   __ldcg(io.node_extra + tbb + to));
+        __stcg(io.lat_extra + k, x < 0.0 ? 0.0 : x);
     }
 }
 
