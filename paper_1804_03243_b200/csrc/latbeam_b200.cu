@@ -528,7 +528,7 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
 // One wave in the frame-synchronous batched mode (lb_batched.cuh): 6-7 phase
 // kernels per frame over all nw lanes, launched back to back on the stream.
 int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T,
-                       int bpl, cudaStream_t st, lb_result *res);
+                       int bpl, cudaStream_t st, lb_result *res, int l0 = 0);
 
 // The per-frame launch sequence is captured once into a CUDA graph and replayed:
 // ~7 launches per frame would otherwise cost more CPU time than a small batch's
@@ -539,6 +539,7 @@ int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &
     int tmax = 0;
     for (int l = 0; l < nw; l++) tmax = std::max(tmax, (int)T[l]);
     std::string key((const char *)&p, sizeof(Params));
+    key += std::string(getenv("LB_GROUPS") ? getenv("LB_GROUPS") : "-") + "/";
     key += std::to_string(nw) + "/" + std::to_string(tmax) + "/" + std::to_string(bpl) + "/" +
            std::to_string((unsigned long long)(uintptr_t)w.d_lanes) + "/" +
            std::to_string((unsigned long long)(uintptr_t)w.d_ctl) + "/" +
@@ -552,7 +553,36 @@ int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         lb_result dummy;
-        const int rc = launch_batched_seq(g, gd, p, w, nw, T, bpl, cs, &dummy);
+        // lane groups on forked streams: independent chains in the graph, so one
+        // group's latency-bound epsilon rounds overlap another group's throughput
+        // phases (the overlap the persistent-lane kernel gets for free)
+        const char *ge = getenv("LB_GROUPS");
+        const int groups = std::max(1, std::min(nw, ge ? atoi(ge) : (nw >= 16 ? 4 : nw >= 8 ? 2 : 1)));
+        int rc = LB_OK;
+        if (groups == 1) {
+            rc = launch_batched_seq(g, gd, p, w, nw, T, bpl, cs, &dummy);
+        } else {
+            cudaEvent_t fork;
+            CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+            CK(cudaEventRecord(fork, cs));
+            std::vector<cudaStream_t> ss(groups);
+            std::vector<cudaEvent_t> joins(groups);
+            for (int q = 0; q < groups; q++) {
+                const int a = nw * q / groups, b = nw * (q + 1) / groups;
+                CK(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
+                CK(cudaStreamWaitEvent(ss[q], fork, 0));
+                const int bq = std::max(1, (g->sms * 4) / std::max(1, b - a));
+                if (!rc) rc = launch_batched_seq(g, gd, p, w, b - a, T + a, bq, ss[q], &dummy, a);
+                CK(cudaEventCreateWithFlags(&joins[q], cudaEventDisableTiming));
+                CK(cudaEventRecord(joins[q], ss[q]));
+                CK(cudaStreamWaitEvent(cs, joins[q], 0));
+            }
+            for (int q = 0; q < groups; q++) {
+                cudaEventDestroy(joins[q]);
+                cudaStreamDestroy(ss[q]);
+            }
+            cudaEventDestroy(fork);
+        }
         cudaGraph_t graph;
         const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
         cudaStreamDestroy(cs);
@@ -569,12 +599,12 @@ int launch_batched(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &
 }
 
 int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspace &w, int nw, const int32_t *T,
-                       int bpl, cudaStream_t st, lb_result *res) {
+                       int bpl, cudaStream_t st, lb_result *res, int l0) {
     int tmax = 0;
     for (int l = 0; l < nw; l++) tmax = std::max(tmax, (int)T[l]);
-    const LaneWs *lw = w.d_lanes;
-    const UttDesc *ud = w.d_desc;
-    LaneCtl *ctl = w.d_ctl;
+    const LaneWs *lw = w.d_lanes + l0;     // this lane group's slice (l0 = first lane)
+    const UttDesc *ud = w.d_desc + l0;
+    LaneCtl *ctl = w.d_ctl + l0;
     const dim3 grid((unsigned)bpl, (unsigned)nw);
     constexpr int ENT = 512, ECL = 2, FNT = 512;
     cudaLaunchConfig_t ec = {};
@@ -668,11 +698,11 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
     // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
-    // CUDA graph) spread every phase over all SMs and win for small batches
-    // (1 utterance: 17.8k vs 8.1k frames/s; 32: 264k vs 225k); the
-    // persistent-lane kernel overlaps the lanes' phases and wins from ~48
-    // concurrent utterances up (64: 388k vs 333k frames/s; C2 graph, measured).
-    // LB_MODE=lane|batched overrides.
+    // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
+    // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
+    // 32: 310k vs 225k; 56: 372k vs 357k); the persistent-lane kernel wins from
+    // ~60 concurrent utterances up (64: 388k vs 375k frames/s; C2 graph,
+    // measured).  LB_MODE=lane|batched overrides.
     const char *mode_env = getenv("LB_MODE");
     bool batched = n <= BATCHED_MAX_UTTS;
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;
