@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <charconv>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -20,6 +21,7 @@
 #include "lb_kernels.cuh"
 #include "lb_lattice.cuh"
 #include "lb_batched.cuh"
+#include "lb_graph_build.cuh"
 
 using namespace lbk;
 
@@ -987,58 +989,30 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
-    // host-side packing of the device layout
-    std::vector<int4> arcs((size_t)A);
-    std::vector<unsigned> hsrc((size_t)A), hol((size_t)A), hoff((size_t)S + 1), heoff((size_t)S + 1);
-    std::vector<int4> heps;
-    int32_t maxil = 0;
-    for (int64_t s = 0; s < S; s++) {
-        hoff[s] = (unsigned)off[s];
-        heoff[s] = (unsigned)heps.size();
-        if (off[s + 1] < off[s]) return set_err(LB_USAGE, "arc offsets must be non-decreasing");
-        for (int64_t a = off[s]; a < off[s + 1]; a++) {
-            if (il[a] == 0) {
-                long long bits;
-                std::memcpy(&bits, &w[a], 8);
-                int4 r;
-                r.x = dst[a];
-                r.y = (int)a;
-                r.z = (int)(bits & 0xFFFFFFFFll);
-                r.w = (int)(bits >> 32);
-                heps.push_back(r);
-            }
-        }
-    }
-    hoff[S] = (unsigned)A;
-    heoff[S] = (unsigned)heps.size();
-    for (int64_t a = 0; a < A; a++) {
-        if (dst[a] < 0 || dst[a] >= S || il[a] < 0 || ol[a] < 0)
-            return set_err(LB_USAGE, "arc field out of range");
-        if (!(std::isfinite(w[a]) && w[a] >= 0.0)) return set_err(LB_USAGE, "arc weight must be finite and >= 0");
-        int4 r;
-        r.x = dst[a];
-        r.y = il[a];
-        long long bits;
-        std::memcpy(&bits, &w[a], 8);
-        r.z = (int)(bits & 0xFFFFFFFFll);
-        r.w = (int)(bits >> 32);
-        arcs[a] = r;
-        hsrc[a] = (unsigned)src[a];
-        hol[a] = (unsigned)ol[a];
-        maxil = std::max(maxil, il[a]);
-    }
-    g->max_ilabel = maxil;
-    g->E = (int64_t)heps.size();
-    // emitting-arc statistics (candidate buffer bound) and the "dst owns epsilon
-    // arcs" flag in bit 31 of the ilabel word (lb_device.cuh EPS_FLAG)
-    for (int64_t s = 0; s < S; s++) {
-        int64_t d = 0;
-        for (int64_t a = off[s]; a < off[s + 1]; a++) d += il[a] != 0;
-        g->A_emit += d;
-        g->max_edeg = std::max(g->max_edeg, d);
-    }
-    for (int64_t a = 0; a < A; a++)
-        if (heoff[dst[a] + 1] > heoff[dst[a]]) arcs[a].y = (int)((unsigned)arcs[a].y | EPS_FLAG);
+    // Upload the CSR columns as they are and build the device layout on the GPU
+    // (lb_graph_build.cuh); raw columns not kept by the replica are freed after.
+    cudaStream_t st = g->stream;
+    long long *d_off = nullptr;
+    int *d_dst = nullptr, *d_il = nullptr;
+    double *d_w = nullptr;
+    unsigned *d_ecnt = nullptr, *d_emit = nullptr, *d_err = nullptr;
+    int *d_maxil = nullptr;
+    unsigned long long *d_sum = nullptr;
+    void *d_tmp = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_off); cudaFree(d_dst); cudaFree(d_il); cudaFree(d_w); cudaFree(d_ecnt); cudaFree(d_emit);
+        cudaFree(d_err); cudaFree(d_maxil); cudaFree(d_sum); cudaFree(d_tmp);
+    };
+    struct Guard { std::function<void()> f; ~Guard() { f(); } } guard{cleanup};
+    CK(dalloc(&d_off, S + 1));
+    CK(dalloc(&d_dst, A));
+    CK(dalloc(&d_il, A));
+    CK(dalloc(&d_w, A));
+    CK(dalloc(&d_ecnt, S + 1));
+    CK(dalloc(&d_emit, S));
+    CK(dalloc(&d_err, 1));
+    CK(dalloc(&d_maxil, 1));
+    CK(dalloc(&d_sum, 2));
     CK(dalloc(&g->arcs, A));
     CK(dalloc(&g->src, A));
     CK(dalloc(&g->ol, A));
@@ -1046,22 +1020,57 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     CK(dalloc(&g->rng, S));
     CK(dalloc(&g->erng, S));
     CK(dalloc(&g->eoff, S + 1));
-    CK(dalloc(&g->eps, g->E));
     CK(dalloc(&g->fin, S));
-    CK(cudaMemcpy(g->arcs, arcs.data(), sizeof(int4) * A, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g->src, hsrc.data(), 4 * A, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g->ol, hol.data(), 4 * A, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g->off, hoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
-    {
-        std::vector<uint2> hr((size_t)S);
-        for (int64_t s = 0; s < S; s++) hr[s] = make_uint2(hoff[s], hoff[s + 1]);
-        CK(cudaMemcpy(g->rng, hr.data(), sizeof(uint2) * S, cudaMemcpyHostToDevice));
-        for (int64_t s = 0; s < S; s++) hr[s] = make_uint2(heoff[s], heoff[s + 1]);
-        CK(cudaMemcpy(g->erng, hr.data(), sizeof(uint2) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(d_off, off, 8 * (S + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_dst, dst, 4 * A, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_il, il, 4 * A, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_w, w, 8 * A, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g->src, src, 4 * A, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g->ol, ol, 4 * A, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g->fin, fin, 8 * S, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_err, 0, 4, st));
+    CK(cudaMemsetAsync(d_maxil, 0, 4, st));
+    const int nb = g->sms * 8;
+    gb_state_pass<<<nb, 256, 0, st>>>(d_off, d_il, S, g->off, g->rng, d_ecnt, d_emit, d_err);
+    // epsilon CSR offsets, emitting-arc total and max out-degree
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, d_ecnt, g->eoff, (int)(S + 1), st));
+    CK(cub::DeviceReduce::Sum(nullptr, t2, d_emit, d_sum, (int)S, st));
+    CK(cub::DeviceReduce::Max(nullptr, t3, d_emit, d_sum + 1, (int)S, st));
+    CK(dalloc((char **)&d_tmp, std::max(t1, std::max(t2, t3))));
+    size_t tt = std::max(t1, std::max(t2, t3));
+    CK(cub::DeviceScan::ExclusiveSum(d_tmp, tt, d_ecnt, g->eoff, (int)(S + 1), st));
+    tt = std::max(t1, std::max(t2, t3));
+    CK(cub::DeviceReduce::Sum(d_tmp, tt, d_emit, d_sum, (int)S, st));
+    tt = std::max(t1, std::max(t2, t3));
+    CK(cub::DeviceReduce::Max(d_tmp, tt, d_emit, d_sum + 1, (int)S, st));
+    unsigned hE = 0, herr = 0;
+    unsigned long long hsum[2] = {0, 0};
+    CK(cudaMemcpyAsync(&hE, g->eoff + S, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hsum, d_sum, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (herr & GB_BAD_OFFSETS) {
+        lb_graph_destroy(g.release());
+        return set_err(LB_USAGE, "arc offsets must be non-decreasing");
     }
-    CK(cudaMemcpy(g->eoff, heoff.data(), 4 * (S + 1), cudaMemcpyHostToDevice));
-    if (g->E) CK(cudaMemcpy(g->eps, heps.data(), sizeof(int4) * g->E, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(g->fin, fin, 8 * S, cudaMemcpyHostToDevice));
+    g->E = hE;
+    g->A_emit = (int64_t)hsum[0];
+    g->max_edeg = (int64_t)(unsigned)hsum[1];
+    CK(dalloc(&g->eps, g->E));
+    gb_state_eps<<<nb, 256, 0, st>>>(d_off, d_il, d_dst, d_w, S, g->eoff, g->eps, g->erng);
+    gb_arcs<<<nb, 256, 0, st>>>(d_dst, d_il, (const int *)g->ol, d_w, A, S, g->erng, g->arcs, d_err, d_maxil);
+    CK(cudaGetLastError());
+    int hmaxil = 0;
+    CK(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hmaxil, d_maxil, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (herr & (GB_BAD_FIELD | GB_BAD_WEIGHT)) {
+        lb_graph_destroy(g.release());
+        return set_err(LB_USAGE, (herr & GB_BAD_FIELD) ? "arc field out of range"
+                                                       : "arc weight must be finite and >= 0");
+    }
+    g->max_ilabel = hmaxil;
     g->bytes = A * 16 + A * 8 + (S + 1) * 8 + 2 * S * 8 + g->E * 16 + S * 8;
     *out = g.release();
     return LB_OK;
