@@ -126,6 +126,21 @@ int lb_result_phases(const lb_result *r, double *ms8);
 int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8);
 void lb_result_free(lb_result *r);
 
+/* Lattice oracle word error (scoring.py:66-114), many lattices at once, one
+ * CTA each.  A lattice view is the FinalLattice columns.  When node_frame is
+ * non-decreasing (nodes numbered by (frame, index)) and every arc stays in its
+ * frame or advances one frame -- what the decoder produces -- the DP walks the
+ * frames in order; otherwise (or node_frame NULL) it relaxes all arcs to a
+ * fixpoint, like the reference.  Arcs may come in any order.
+ * errors[i] = fewest word errors, -1 = no complete path, -2 = no convergence.
+ * Returns LB_USAGE for an empty reference or out-of-range ids. */
+typedef struct {
+    int64_t num_nodes, start, n_final, n_arcs, n_ref;
+    const int64_t *final_ids, *from, *to, *olabel, *node_frame;
+    const int32_t *ref;
+} lb_lattice_view;
+int lb_oracle_wer_batch(int32_t device, int32_t n, const lb_lattice_view *lats, int64_t *errors);
+
 /* write_lattice_text (lattice.py:605-614) in native code, byte-identical to the
  * reference's text (floats as Python repr): returns the text length; the text
  * is written to buf only if cap >= that length.  Host-only, no device needed. */

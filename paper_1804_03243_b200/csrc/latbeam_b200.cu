@@ -22,6 +22,7 @@
 #include "lb_lattice.cuh"
 #include "lb_batched.cuh"
 #include "lb_graph_build.cuh"
+#include "lb_scoring.cuh"
 
 using namespace lbk;
 
@@ -1341,6 +1342,121 @@ int lb_result_warp_phases(const lb_result *r, double *busy_ms8, double *samples8
 }
 
 void lb_result_free(lb_result *r) { delete r; }
+
+int lb_oracle_wer_batch(int32_t device, int32_t n, const lb_lattice_view *lats, int64_t *errors) {
+    if (n < 0 || (n > 0 && (!lats || !errors))) return set_err(LB_USAGE, "bad arguments");
+    if (n == 0) return LB_OK;
+    CK(cudaSetDevice(device));
+    // host: frame node ranges and from-frame arc ranges, packed per job
+    std::vector<WerJob> jobs(n);
+    std::vector<std::vector<int>> packs(n);
+    size_t total_best = 0;
+    for (int i = 0; i < n; i++) {
+        const lb_lattice_view &L = lats[i];
+        if (L.n_ref < 1) return set_err(LB_USAGE, "reference word sequence is empty");
+        if (L.num_nodes < 1 || L.start < 0 || L.start >= L.num_nodes)
+            return set_err(LB_USAGE, "bad lattice dimensions");
+        const int64_t N = L.num_nodes, M = L.n_arcs;
+        // arcs in from-node order (stable), as scoring.py:80-83 sweeps them
+        std::vector<int64_t> ord(M);
+        for (int64_t k = 0; k < M; k++) ord[k] = k;
+        bool sorted = true;
+        for (int64_t k = 1; k < M && sorted; k++) sorted = L.from[k] >= L.from[k - 1];
+        if (!sorted) std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return L.from[a] < L.from[b]; });
+        for (int64_t k = 0; k < M; k++) {
+            if (L.from[k] < 0 || L.from[k] >= N || L.to[k] < 0 || L.to[k] >= N)
+                return set_err(LB_USAGE, "lattice arc endpoint out of range");
+        }
+        for (int64_t q = 0; q < L.n_final; q++)
+            if (L.final_ids[q] < 0 || L.final_ids[q] >= N) return set_err(LB_USAGE, "final node id out of range");
+        // frame-ordered DP when node ids are in frame order and every arc stays in
+        // its frame or steps to the next one (all decoder lattices); otherwise the
+        // whole lattice is one "frame" and the in-frame fixpoint is a plain
+        // Bellman-Ford over all arcs -- same distances, more rounds.
+        bool framed = L.node_frame != nullptr;
+        for (int64_t v = 0; framed && v < N; v++)
+            framed = L.node_frame[v] >= 0 && (v == 0 || L.node_frame[v] >= L.node_frame[v - 1]);
+        for (int64_t k = 0; framed && k < M; k++) {
+            const int64_t df = L.node_frame[L.to[k]] - L.node_frame[L.from[k]];
+            framed = df == 0 || df == 1;
+        }
+        int F = 1;
+        std::vector<int> nb, ab;
+        if (framed) {
+            F = (int)L.node_frame[N - 1] + 1;
+            nb.assign(F + 1, 0);
+            ab.assign(F + 1, 0);
+            for (int64_t v = 0, f = 0; f <= F; f++) {
+                while (v < N && L.node_frame[v] < f) v++;
+                nb[f] = (int)v;
+            }
+            for (int64_t f = 0, k = 0; f <= F; f++) {
+                while (k < M && L.from[ord[k]] < nb[f]) k++;
+                ab[f] = (int)k;
+            }
+        } else {
+            nb = {0, (int)N};
+            ab = {0, (int)M};
+        }
+        std::vector<int> afrom(M), ato(M), aol(M);
+        for (int64_t k = 0; k < M; k++) {
+            afrom[k] = (int)L.from[ord[k]];
+            ato[k] = (int)L.to[ord[k]];
+            aol[k] = (int)L.olabel[ord[k]];
+        }
+        std::vector<int> &pk = packs[i];
+        auto put = [&](const auto &src, int64_t cnt) {
+            size_t o = pk.size();
+            for (int64_t k = 0; k < cnt; k++) pk.push_back((int)src[k]);
+            return o;
+        };
+        const size_t o_from = put(afrom.data(), M), o_to = put(ato.data(), M), o_ol = put(aol.data(), M);
+        const size_t o_nb = put(nb.data(), F + 1), o_ab = put(ab.data(), F + 1);
+        const size_t o_fin = put(L.final_ids, L.n_final), o_ref = put(L.ref, L.n_ref);
+        WerJob &J = jobs[i];
+        J.num_nodes = (int)N;
+        J.start = (int)L.start;
+        J.n_final = (int)L.n_final;
+        J.F = F;
+        J.r = (int)L.n_ref;
+        // offsets for now; made device pointers after upload
+        J.from = (const int *)o_from; J.to = (const int *)o_to; J.ol = (const int *)o_ol;
+        J.nb = (const int *)o_nb; J.ab = (const int *)o_ab; J.finals = (const int *)o_fin; J.ref = (const int *)o_ref;
+        J.best = (int *)total_best;
+        total_best += (size_t)N * (L.n_ref + 1);
+    }
+    size_t total_pack = 0;
+    for (auto &pk : packs) total_pack += pk.size();
+    int *d_pack = nullptr, *d_best = nullptr;
+    long long *d_out = nullptr;
+    WerJob *d_jobs = nullptr;
+    CK(dalloc(&d_pack, total_pack));
+    CK(dalloc(&d_best, total_best));
+    CK(dalloc(&d_out, n));
+    CK(dalloc(&d_jobs, n));
+    size_t base = 0;
+    for (int i = 0; i < n; i++) {
+        CK(cudaMemcpy(d_pack + base, packs[i].data(), 4 * packs[i].size(), cudaMemcpyHostToDevice));
+        WerJob &J = jobs[i];
+        auto rebase = [&](const int *o) { return (const int *)(d_pack + base + (size_t)o); };
+        J.from = rebase(J.from); J.to = rebase(J.to); J.ol = rebase(J.ol); J.nb = rebase(J.nb);
+        J.ab = rebase(J.ab); J.finals = rebase(J.finals); J.ref = rebase(J.ref);
+        J.best = d_best + (size_t)J.best;
+        J.out = d_out + i;
+        base += packs[i].size();
+    }
+    CK(cudaMemcpy(d_jobs, jobs.data(), sizeof(WerJob) * n, cudaMemcpyHostToDevice));
+    oracle_wer_kernel<<<n, 1024>>>(d_jobs, n);
+    CK(cudaGetLastError());
+    std::vector<long long> out(n);
+    CK(cudaMemcpy(out.data(), d_out, 8 * n, cudaMemcpyDeviceToHost));
+    cudaFree(d_pack);
+    cudaFree(d_best);
+    cudaFree(d_out);
+    cudaFree(d_jobs);
+    for (int i = 0; i < n; i++) errors[i] = out[i];
+    return LB_OK;
+}
 
 int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const int64_t *final_ids,
                         const double *final_costs, int64_t n_arcs, const int64_t *from, const int64_t *to,

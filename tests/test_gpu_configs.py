@@ -17,6 +17,8 @@ real-length utterances:
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import pytest
 
@@ -81,6 +83,30 @@ def test_c2_c3_full_utterance(oracle_mod, name, want_lattice):
     # max-active binds on this graph: the cap is reached on most frames
     sizes = np.asarray([len(s) for s, _ in got.frame_packs[1:]])
     assert np.median(sizes) >= 0.9 * d["max_active"], np.median(sizes)
+
+
+def test_c3_lattice_oracle_wer_on_gpu():
+    """Full-size C3 lattice (HCLG graph, epsilon arcs, lattice beam 8): GPU oracle
+    WER vs the CPU restatement of scoring.py:66-114, against a reference made
+    from the 1-best words with seeded edits."""
+    from oracle import scoring_oracle as SO
+    w = graph("C3")
+    d = synthetic.CONFIGS["C3"]["decode"]
+    r = lb.decode_utterance(w, synthetic.config_matrix("C3", 0),
+                            lb.DecodeConfig(beam=d["beam"], lattice_beam=d["lattice_beam"],
+                                            max_active=d["max_active"], max_lattice_arcs=50_000_000))
+    fl = r.lattice
+    assert fl.num_arcs > 10000
+    rng = np.random.default_rng(9)
+    ref = [x if rng.random() < 0.7 else int(rng.integers(1, 1000)) for x in r.words[:12]] or [1]
+    t0 = time.perf_counter()
+    got = lb.oracle_wer(fl, ref)
+    print(f"C3 lattice {fl.num_nodes} nodes {fl.num_arcs} arcs: gpu oracle_wer {time.perf_counter() - t0:.3f}s")
+    t0 = time.perf_counter()
+    want = SO.oracle_wer(fl.num_nodes, fl.start, fl.final_ids, fl.from_, fl.to, fl.olabel, ref)
+    print(f"cpu restatement {time.perf_counter() - t0:.3f}s")
+    assert got == want
+    assert got <= lb.wer(r.words, ref).errors
 
 
 def test_c4_batch_of_64_lanes(oracle_mod):
