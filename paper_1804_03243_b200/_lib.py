@@ -14,7 +14,8 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "liblatbeam_b200.so")
+# LB_SO_PATH: load a variant build (tools/variants.sh experiments only)
+SO_PATH = os.environ.get("LB_SO_PATH") or os.path.join(_HERE, "liblatbeam_b200.so")
 
 P64, P32, PD, PU64, PV = (C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_double),
                           C.POINTER(C.c_uint64), C.c_void_p)

@@ -76,22 +76,91 @@ struct __align__(32) StateRec {
     double minsnap;
 };
 
+
+// ---- per-state (lane-private, reused frame to frame) accesses: L2 policy ----
+// The record/epsilon arrays are accessed with an L2 evict_last cache policy so
+// the streamed candidate and token arrays (evict-first) do not push the hot
+// state records out of L2 (C4: +3 %; LB_NO_L2HINT builds without it).
+#ifndef LB_NO_L2HINT
+#define LB_L2HINT 1
+#endif
+#ifdef LB_L2HINT
+__device__ __forceinline__ unsigned long long l2_pol() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+#endif
+
+__device__ __forceinline__ unsigned long long rld_u64(const unsigned long long *a) {
+    unsigned long long v;
+#ifdef LB_L2HINT
+    asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(l2_pol()));
+#else
+    v = __ldcg(a);
+#endif
+    return v;
+}
+__device__ __forceinline__ double rld_f64(const double *a) {
+    return __longlong_as_double((long long)rld_u64(reinterpret_cast<const unsigned long long *>(a)));
+}
+__device__ __forceinline__ int rld_i32(const int *a) {
+    int v;
+#ifdef LB_L2HINT
+    asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(l2_pol()));
+#else
+    v = __ldcg(a);
+#endif
+    return v;
+}
+__device__ __forceinline__ void rst_u64(unsigned long long *a, unsigned long long v) {
+#ifdef LB_L2HINT
+    asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(l2_pol()) : "memory");
+#else
+    __stcg(a, v);
+#endif
+}
+__device__ __forceinline__ void rst_f64(double *a, double v) {
+    rst_u64(reinterpret_cast<unsigned long long *>(a), (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ ulonglong2 rld_u128(const void *a) {
+    ulonglong2 v;
+#ifdef LB_L2HINT
+    asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(a), "l"(l2_pol()));
+#else
+    v = __ldcg(reinterpret_cast<const ulonglong2 *>(a));
+#endif
+    return v;
+}
+__device__ __forceinline__ void rst_u128(void *a, ulonglong2 v) {
+#ifdef LB_L2HINT
+    asm volatile("st.global.cg.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(a), "l"(v.x), "l"(v.y), "l"(l2_pol()) : "memory");
+#else
+    __stcg(reinterpret_cast<ulonglong2 *>(a), v);
+#endif
+}
+
 // A winner's {cost, pred, tokidx = -1} in one 16-byte store (the stale token
 // index of an older frame is dead once the frame's emit barrier has passed).
 __device__ __forceinline__ void store_winner(StateRec *r, double cost, int pred) {
     const unsigned long long hi = (unsigned long long)(unsigned)pred | 0xFFFFFFFF00000000ull;
-    asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(r),
-                 "l"((unsigned long long)__double_as_longlong(cost)), "l"(hi)
-                 : "memory");
+    rst_u128(r, make_ulonglong2((unsigned long long)__double_as_longlong(cost), hi));
 }
 // The whole record in one 32-byte store.
 __device__ __forceinline__ void store_rec32(StateRec *r, double cost, int pred, int tokidx,
                                             unsigned long long pack, double minsnap) {
     const unsigned long long x1 = (unsigned long long)(unsigned)pred | ((unsigned long long)(unsigned)tokidx << 32);
+#ifdef LB_L2HINT
+    asm volatile("st.global.cg.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(r),
+                 "l"((unsigned long long)__double_as_longlong(cost)), "l"(x1), "l"(pack),
+                 "l"((unsigned long long)__double_as_longlong(minsnap)), "l"(l2_pol())
+                 : "memory");
+#else
     asm volatile("st.global.cg.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(r),
                  "l"((unsigned long long)__double_as_longlong(cost)), "l"(x1), "l"(pack),
                  "l"((unsigned long long)__double_as_longlong(minsnap))
                  : "memory");
+#endif
 }
 
 // Round-local epsilon winner of a state: the min improving offer's word and the
@@ -105,6 +174,15 @@ struct __align__(16) EpsWin {
 // Per-lane scratch.  O(S) arrays are allocated once and reset
 // O(touched) per frame.  Lists marked [C] have one S-sized segment per CTA of
 // the lane (CTA-local append counters in shared memory, no DSMEM traffic).
+// candidate buffer cache policy: streamed (evict-first) by default
+#ifdef LB_CAND_CG
+#define CAND_ST __stcg
+#define CAND_LD __ldcg
+#else
+#define CAND_ST __stcs
+#define CAND_LD __ldcs
+#endif
+
 struct LaneWs {
     StateRec *rec;             // [S]
     EpsWin *rpk;               // [2][S] epsilon round winners by round parity
@@ -185,8 +263,13 @@ struct RecView {
 };
 __device__ __forceinline__ RecView load_rec32(const StateRec *r) {
     unsigned long long x0, x1, x2, x3;
+#ifdef LB_L2HINT
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(r), "l"(l2_pol()));
+#else
     asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(r));
+#endif
     RecView v;
     v.cost = __longlong_as_double((long long)x0);
     v.pred = (int)(unsigned)(x1 & 0xFFFFFFFFull);
@@ -228,18 +311,30 @@ __device__ __forceinline__ void epswin_min(EpsWin *p, unsigned long long word, d
 // atomicMin would carry a shared-memory CAS fallback path).
 __device__ __forceinline__ unsigned long long atom_min_u64(unsigned long long *a, unsigned long long v) {
     unsigned long long o;
+#ifdef LB_L2HINT
+    asm volatile("atom.relaxed.gpu.global.min.L2::cache_hint.u64 %0, [%1], %2, %3;" : "=l"(o) : "l"(a), "l"(v), "l"(l2_pol()) : "memory");
+#else
     asm volatile("atom.relaxed.gpu.global.min.u64 %0, [%1], %2;" : "=l"(o) : "l"(a), "l"(v) : "memory");
+#endif
     return o;
 }
 __device__ __forceinline__ unsigned atom_exch_u32(unsigned *a, unsigned v) {
     unsigned o;
+#ifdef LB_L2HINT
+    asm volatile("atom.relaxed.gpu.global.exch.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(l2_pol()) : "memory");
+#else
     asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(a), "r"(v) : "memory");
+#endif
     return o;
 }
 
 // Fire-and-forget 64-bit min at L2 (REDG): the issuing thread never waits.
 __device__ __forceinline__ void red_min_u64(unsigned long long *a, unsigned long long v) {
+#ifdef LB_L2HINT
+    asm volatile("red.relaxed.gpu.global.min.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(l2_pol()) : "memory");
+#else
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+#endif
 }
 
 __device__ __forceinline__ void load_arc(const int4 *arcs, unsigned a, unsigned &dst, unsigned &il,

@@ -238,8 +238,16 @@ __device__ __forceinline__ int hist_bin(double c, double best, double width, dou
 // Per-lane decode phases.  UNR = independent arcs per thread per emit batch.
 template <int UNR>
 struct Lane {
+#ifdef LB_WUNR
+    static constexpr int WUNR = LB_WUNR;
+#else
     static constexpr int WUNR = UNR; // candidates per thread per winners batch
-    static constexpr int AUNR = 2;   // touched states per thread per aggregate batch
+#endif
+#ifdef LB_AUNR
+    static constexpr int AUNR = LB_AUNR;
+#else
+    static constexpr int AUNR = 1;   // touched states per thread per aggregate batch (2 spills at 80 regs)
+#endif
     static constexpr int EUNR = 2;   // frontier entries per thread per epsilon batch
     const GraphDev &g;      // __grid_constant__ kernel parameters: referenced in place,
     const Params &p;        // never copied to local memory
@@ -349,7 +357,7 @@ struct Lane {
         if (threadIdx.x == 0) lane_sm.nfr[0] = lane_sm.nfr[1] = lane_sm.nfr[2] = 0;
         const unsigned long long t0 = wbegin();
         auto fill_tail = [&]() {
-            for (int i = cused + lane; i < CCH; i += 32) __stcs(cb + cstart + i, make_int4(-1, 0, 0, 0));
+            for (int i = cused + lane; i < CCH; i += 32) CAND_ST(cb + cstart + i, make_int4(-1, 0, 0, 0));
         };
         for_each_token_arc_batched<UNR>(g, G.gwarp(), G.gnw(), pts, ptc, np, c_scan, wmap(),
                                         [&](const bool *vv, const int *ii, const unsigned *aa, const double *cc) {
@@ -417,9 +425,9 @@ struct Lane {
                         const long long bits = __double_as_longlong(cand[u]);
                         const unsigned flag = (unsigned)r[u].y & EPS_FLAG;
                         const int k = cstart + cused + off[u];
-                        __stcs(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
+                        CAND_ST(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
                                                  (int)(bits & 0xFFFFFFFFll), (int)(bits >> 32)));
-                        __stcs(cbi + k, ii[u]);
+                        CAND_ST(cbi + k, ii[u]);
                     }
                 }
             }
@@ -453,7 +461,7 @@ struct Lane {
         for (int q = threadIdx.x; q < mine; q += blockDim.x) {
             const long long o = tbf + (long long)__ldcg(fx + q);
             const int u = __ldcg(io.tok_pred + o) >> 1;
-            const int pi = __ldcg(&L.rec[u].tokidx);
+            const int pi = rld_i32(&L.rec[u].tokidx);
             if (pi < 0 || pi >= nf || __ldcg(io.tok_state + tbf + pi) != (unsigned)u)
                 set_error(E_INT_EPS_PRED, frame, u);
             __stcg(io.tok_pred + o, pi << 1);
@@ -498,7 +506,7 @@ struct Lane {
                 unsigned long long pk[WUNR];
 #pragma unroll
                 for (int u = 0; u < WUNR; u++)
-                    pk[u] = e[u].x != -1 ? __ldcg(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
+                    pk[u] = e[u].x != -1 ? rld_u64(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
 #pragma unroll
                 for (int u = 0; u < WUNR; u++)
                     nown += e[u].x != -1 && pk[u] == pack_word(__hiloint2double(e[u].w, e[u].z), (unsigned)e[u].y);
@@ -514,14 +522,14 @@ struct Lane {
                 const int k = kb + u * 32 + lane;
                 e[u].x = -1;
                 if (k < nc) {
-                    e[u] = __ldcs(cb + k);
-                    if (e[u].x != -1) ti[u] = __ldcs(cbi + k);
+                    e[u] = CAND_LD(cb + k);
+                    if (e[u].x != -1) ti[u] = CAND_LD(cbi + k);
                 }
             }
             unsigned long long pk[WUNR];
 #pragma unroll
             for (int u = 0; u < WUNR; u++)
-                pk[u] = e[u].x != -1 ? __ldcg(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
+                pk[u] = e[u].x != -1 ? rld_u64(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
 #pragma unroll
             for (int u = 0; u < WUNR; u++) {
                 const unsigned v = (unsigned)e[u].x & ~EPS_FLAG;
@@ -656,10 +664,10 @@ struct Lane {
                     if (v[u] == 0xFFFFFFFFu) continue;
                     er[u] = __ldg(g.erng + v[u]);
                     if (r == 0) {
-                        c[u] = __ldcg(&rec[v[u]].cost);
+                        c[u] = rld_f64(&rec[v[u]].cost);
                     } else {
-                        const ulonglong2 w2 = __ldcg(reinterpret_cast<const ulonglong2 *>(rprev + v[u]));
-                        __stcg(reinterpret_cast<ulonglong2 *>(rprev + v[u]), make_ulonglong2(~0ull, ~0ull));
+                        const ulonglong2 w2 = rld_u128(rprev + v[u]);
+                        rst_u128(rprev + v[u], make_ulonglong2(~0ull, ~0ull));
                         c[u] = __longlong_as_double((long long)w2.y);
                         const unsigned src = __ldg(g.src + (unsigned)w2.x);
                         store_winner(&rec[v[u]], c[u], (int)(src << 1));
@@ -671,8 +679,8 @@ struct Lane {
                     if (!(c[u] <= cutoff)) continue;      // round-0 seeds above a max-active cutoff
                     c_front++;
                     if (LAT) {
-                        const double m = __ldcg(&rec[v[u]].minsnap);
-                        if (c[u] < m) __stcg(&rec[v[u]].minsnap, c[u]);
+                        const double m = rld_f64(&rec[v[u]].minsnap);
+                        if (c[u] < m) rst_f64(&rec[v[u]].minsnap, c[u]);
                     }
                     c_escan += er[u].y - er[u].x;
                     for (unsigned e = er[u].x; e < er[u].y; ++e) {
@@ -774,7 +782,7 @@ struct Lane {
                 store_rec32(&rec[v], c, pr, idx, SENT, st.msnap[i]);
                 fx = !init && (pr & 1) == 0;
             } else if (i < st.n) {
-                __stcg(&rec[st.v[i]].pack, SENT);   // over the arena: error raised after the barrier
+                rst_u64(&rec[st.v[i]].pack, SENT);   // over the arena: error raised after the barrier
             }
             sf.push(fx, (unsigned)idx, &lane_sm.nfix[par], fixes());
         }
@@ -808,7 +816,7 @@ struct Lane {
                 const bool valid = v[u] != 0xFFFFFFFFu;
                 const bool init = valid && frame == 0 && (int)v[u] == g.start;
                 const bool keep = valid && (init || rv[u].cost <= cutoff);
-                if (valid && !keep) __stcg(&rec[v[u]].pack, SENT);
+                if (valid && !keep) rst_u64(&rec[v[u]].pack, SENT);
                 const unsigned m = __ballot_sync(FULL, keep);
                 if (keep) {
                     const int j = st.n + __popc(m & lt);
@@ -851,7 +859,7 @@ struct Lane {
     }
 
     __device__ __forceinline__ bool kept(unsigned v, long long tb, int n, int &j) const {
-        j = __ldcg(&L.rec[v].tokidx);
+        j = rld_i32(&L.rec[v].tokidx);
         return j >= 0 && j < n && __ldcg(io.tok_state + tb + j) == v;
     }
 
@@ -880,8 +888,8 @@ struct Lane {
             for (int j = G.gtid(); j < n; j += G.gstride()) {
                 const unsigned u = __ldcg(io.tok_state + tb + j);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                const double ms = __ldcg(&L.rec[u].minsnap);
-                __stcg(&L.rec[u].minsnap, inf);
+                const double ms = rld_f64(&L.rec[u].minsnap);
+                rst_f64(&L.rec[u].minsnap, inf);
                 for (unsigned e = e0; e < e1; ++e) {
                     const int4 r = __ldg(g.eps + e);
                     int jv;
@@ -908,10 +916,10 @@ struct Lane {
         const double inf = inf_d();
         for (int k = threadIdx.x; k < nt; k += blockDim.x) {
             const unsigned v = __ldcg(tl + k);
-            __stcg(&L.rec[v].pack, SENT);
-            __stcg(&L.rec[v].minsnap, inf);
-            __stcg(reinterpret_cast<ulonglong2 *>(rpk(0) + v), make_ulonglong2(~0ull, ~0ull));
-            __stcg(reinterpret_cast<ulonglong2 *>(rpk(1) + v), make_ulonglong2(~0ull, ~0ull));
+            rst_u64(&L.rec[v].pack, SENT);
+            rst_f64(&L.rec[v].minsnap, inf);
+            rst_u128(rpk(0) + v, make_ulonglong2(~0ull, ~0ull));
+            rst_u128(rpk(1) + v, make_ulonglong2(~0ull, ~0ull));
         }
         G.sync();
     }

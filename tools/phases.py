@@ -16,7 +16,8 @@ from paper_1804_03243_b200.resident import decode_batch_resident
 U = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 confs = [tuple(int(x) for x in a.split("x")) for a in (sys.argv[3:] or ["2x768"])]
-g = synthetic.hclg_graph(0)
+import json
+g = synthetic.hclg_graph(0, **json.loads(os.environ.get("LB_GRAPH_KW", "{}")))
 mats = [torch.from_numpy(np.array(synthetic.hclg_matrix(100 + i, num_frames=T).costs)).cuda()
         for i in range(U)]
 names = ("tok", "scan", "cand", "efront", "escan", "ecand", "next", "lat")
