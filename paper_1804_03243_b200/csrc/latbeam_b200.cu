@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -159,6 +160,8 @@ struct lb_graph {
     size_t d_costs_cap = 0;
     double *h_stage = nullptr;
     size_t h_stage_cap = 0;
+    int *h_ready = nullptr;   // progressive staging counter (mapped pinned)
+    int *d_ready = nullptr;
     GraphDev dev() const {
         GraphDev g;
         g.arcs = arcs;
@@ -686,7 +689,7 @@ int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspa
 }
 
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
-                const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms) {
+                const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
     const bool lat = cfg->want_lattice != 0;
     const bool keep_work = lat && cfg->keep_work_lattice != 0;
     const bool packs = cfg->collect_frame_packs != 0 || keep_work;
@@ -754,6 +757,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     p.prof = nullptr;
     const char *ex = getenv("LB_EXP");
     p.exp = ex ? atoi(ex) : 0;
+    p.ready = d_ready;
+    if (batched && d_ready) return set_err(LB_INTERNAL, "progressive staging needs the lane kernel");
     const char *pe = getenv("LB_PHASE_PROFILE");
     unsigned long long *d_prof = nullptr;
     if (pe && pe[0] == '1') {
@@ -1093,6 +1098,7 @@ int lb_graph_destroy(lb_graph *g) {
     cudaFree(g->fin);
     cudaFree(g->d_costs);
     if (g->h_stage) cudaFreeHost(g->h_stage);
+    if (g->h_ready) cudaFreeHost(g->h_ready);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
     return LB_OK;
@@ -1112,9 +1118,9 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     if (g->max_ilabel > D) return set_err(LB_USAGE, "graph uses an input label beyond the cost matrix columns");
     size_t total = 0;
     std::vector<size_t> off(n + 1, 0);
-    for (int i = 0; i < n; i++) {
+    for (int i = 0; i < n; i++) {   // each matrix starts on a 128-byte line (see CF below)
         if (T[i] < 1) return set_err(LB_USAGE, "every cost matrix needs T >= 1");
-        total += (size_t)T[i] * D;
+        total += ((size_t)T[i] * D + 15) & ~(size_t)15;
         off[i + 1] = total;
     }
     std::lock_guard<std::mutex> lock(g->mu);
@@ -1126,47 +1132,97 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
         CK(cudaHostAlloc((void **)&g->h_stage, std::max<size_t>(total, 1) * 8, cudaHostAllocMapped));
         g->h_stage_cap = total;
     }
-    // Stage the caller's matrices into pinned, device-mapped memory with all host
-    // threads (one memcpy thread is ~10 GB/s; the staging copy dominated e2e).
-    const auto t_stage = std::chrono::steady_clock::now();
-    {
-        const size_t bytes = total * 8;
-        unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-        if (bytes < ((size_t)8 << 20)) nth = 1;
-        auto work = [&](unsigned w) {
-            const size_t lo = bytes * w / nth, hi = bytes * (w + 1) / nth;
-            // copy [lo, hi) of the concatenated matrices
-            size_t pos = lo;
-            int i = (int)(std::upper_bound(off.begin(), off.end(), lo / 8) - off.begin()) - 1;
-            while (pos < hi && i < n) {
-                const size_t ub = std::min(hi, off[i + 1] * 8);
-                if (ub > pos) {
-                    std::memcpy(reinterpret_cast<char *>(g->h_stage) + pos,
-                                reinterpret_cast<const char *>(costs[i]) + (pos - off[i] * 8), ub - pos);
-                    pos = ub;
-                }
-                i++;
-            }
-        };
-        std::vector<std::thread> th;
-        for (unsigned w = 1; w < nth; w++) th.emplace_back(work, w);
-        work(0);
-        for (auto &t : th) t.join();
-    }
-    const float stage_ms =
-        std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_stage).count();
-    // 1-best decodes read each frame's row once per lane: the kernel reads the
-    // mapped staging buffer directly (zero-copy, overlapped with decoding).
-    // Lattice decodes re-read rows in the prune pass: copy them to HBM.
-    // (only the persistent-lane kernel reads rows once per frame; the batched mode
-    // gathers acoustic costs per candidate and needs them in HBM)
+    // 1-best decodes in the lane kernel read each frame's row once per lane: the
+    // kernel reads the mapped staging buffer directly (zero-copy).  Lattice decodes
+    // re-read rows in the prune pass, and the batched mode gathers acoustic costs
+    // per candidate: those copy the rows to HBM.
     const char *mode_env = getenv("LB_MODE");
     const bool lane_mode = cfg->want_lattice || (mode_env && !strcmp(mode_env, "lane")) ||
                            (n > BATCHED_MAX_UTTS && !(mode_env && !strcmp(mode_env, "batched")));
     const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
                            !getenv("LB_E2E_COPY");
+    // Stage the caller's matrices into pinned, device-mapped memory with all host
+    // threads (one memcpy thread is ~10 GB/s).  Zero-copy decodes stage
+    // progressively: frame chunks of every utterance in order, each published
+    // through a mapped counter the lanes wait on (Params::ready), so the copy
+    // overlaps the decode instead of preceding it.
+    const size_t bytes = total * 8;
+    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (bytes < ((size_t)8 << 20)) nth = 1;
+    const bool progressive = zero_copy && !getenv("LB_NO_PROGRESSIVE") && n > 0;
+    int tmax = 1;
+    for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
+    // Frames per published chunk.  16 rows of D doubles are 128*D bytes, so with
+    // line-aligned matrices no 128-byte line spans two chunks: a line the kernel
+    // pulls into L2 never holds bytes of a chunk that is not yet published.
+    const int CF = 16;
+    const int nchunks = progressive ? (tmax + CF - 1) / CF : 1;
+    // pieces of chunk c: (destination byte offset, source pointer, bytes)
+    struct Piece { size_t dst; const char *src; size_t len; };
+    std::vector<std::vector<Piece>> chunks(nchunks);
+    std::vector<size_t> chunk_bytes(nchunks, 0);
+    for (int c = 0; c < nchunks; c++) {
+        for (int i = 0; i < n; i++) {
+            const int f0 = progressive ? c * CF : 0, f1 = progressive ? std::min<int>(T[i], (c + 1) * CF) : T[i];
+            if (f1 <= f0) continue;
+            const size_t len = (size_t)(f1 - f0) * D * 8;
+            chunks[c].push_back({(off[i] + (size_t)f0 * D) * 8,
+                                 reinterpret_cast<const char *>(costs[i]) + (size_t)f0 * D * 8, len});
+            chunk_bytes[c] += len;
+        }
+    }
+    if (progressive && !g->h_ready) {
+        CK(cudaHostAlloc((void **)&g->h_ready, 64, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void **)&g->d_ready, g->h_ready, 0));
+    }
+    if (progressive) __atomic_store_n(g->h_ready, 0, __ATOMIC_SEQ_CST);
+    std::vector<std::atomic<int>> done(nth);
+    for (auto &d : done) d.store(0);
+    char *stage = reinterpret_cast<char *>(g->h_stage);
+    int *h_ready = g->h_ready;
+    auto work = [&, stage, h_ready](unsigned w) {
+        for (int c = 0; c < nchunks; c++) {
+            // copy bytes [lo, hi) of chunk c's concatenated pieces
+            const size_t lo = chunk_bytes[c] * w / nth, hi = chunk_bytes[c] * (w + 1) / nth;
+            size_t base = 0;
+            for (const Piece &pc : chunks[c]) {
+                const size_t a = std::max(lo, base), b = std::min(hi, base + pc.len);
+                if (a < b) std::memcpy(stage + pc.dst + (a - base), pc.src + (a - base), b - a);
+                base += pc.len;
+                if (base >= hi) break;
+            }
+            done[w].store(c + 1, std::memory_order_seq_cst);   // seq_cst: two finishers must not both miss each other
+            if (progressive) {   // publish the chunks every worker has finished
+                int m = c + 1;
+                for (unsigned q = 0; q < nth; q++) m = std::min(m, done[q].load(std::memory_order_seq_cst));
+                const int frames = m >= nchunks ? tmax : m * CF;
+                int cur = __atomic_load_n(h_ready, __ATOMIC_ACQUIRE);
+                while (cur < frames &&
+                       !__atomic_compare_exchange_n(h_ready, &cur, frames, false, __ATOMIC_RELEASE, __ATOMIC_ACQUIRE)) {
+                }
+            }
+        }
+    };
+    const auto t_stage = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
     std::vector<const double *> dptr(n);
-    float h2d = stage_ms;
+    float h2d = 0.0f;
+    if (progressive) {
+        for (unsigned w = 0; w < nth; w++) th.emplace_back(work, w);
+        double *dev = nullptr;
+        CK(cudaHostGetDevicePointer((void **)&dev, g->h_stage, 0));
+        for (int i = 0; i < n; i++) dptr[i] = dev + off[i];
+        rc = decode_impl(g, n, dptr.data(), T, D, cfg, g->stream, res.get(), 0.0f, g->d_ready);
+        for (auto &t : th) t.join();   // the kernel finished, so every chunk was published
+        res->t_h2d = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_stage).count();
+        if (rc) return rc;
+        *out = res.release();
+        return LB_OK;
+    }
+    for (unsigned w = 1; w < nth; w++) th.emplace_back(work, w);
+    work(0);
+    for (auto &t : th) t.join();
+    h2d = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_stage).count();
     if (zero_copy) {
         double *dev = nullptr;
         CK(cudaHostGetDevicePointer((void **)&dev, g->h_stage, 0));
@@ -1537,6 +1593,7 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     p.D = D;
     p.acrow_smem = 0;
     p.exp = 0;
+    p.ready = nullptr;
     const int esm = (int)lane_dyn_smem(768, 1, false);
     CK(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, esm));
     expand_kernel<<<1, 768, esm, st>>>(g->dev(), p, L, d, (int)n, mode, cutoff);

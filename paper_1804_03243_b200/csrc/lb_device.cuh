@@ -232,6 +232,8 @@ struct Params {
     int acrow_smem;
     unsigned long long *prof;   // optional per-phase ns accumulators (LB_PHASE_PROFILE=1)
     int exp;                    // timing experiments (LB_EXP, profiling only; results not exact)
+    const int *ready;           // progressive host staging (mapped): rows of frames < *ready are
+                                // in place for every utterance; nullptr = all rows ready
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -65,6 +65,7 @@ struct Smem {
     double red[32];
     int ired[32];
     int hist[2][NBINS];            // max-active histogram (frame parity)
+    int ready_seen;                // last value of *Params::ready this CTA observed
 };
 
 // The lane CTA's shared state and dynamic shared memory, declared at namespace
@@ -314,10 +315,35 @@ struct Lane {
         }
     }
 
-    __device__ void load_row(const double *r) {
+    // Frame rows staged progressively by the host (lb_decode_batch, zero-copy):
+    // wait until the rows of frames < need are published.  The smem copy of the
+    // flag is only written between barriers, so the test is CTA-uniform and a
+    // barrier is spent only when the staging is behind (about once per chunk).
+    __device__ void wait_rows(int need) {
+        if (lane_sm.ready_seen >= need) return;
+        if (threadIdx.x == 0) {
+            int r;
+            for (;;) {
+                asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(r) : "l"(p.ready) : "memory");
+                if (r >= need) break;
+                __nanosleep(1000);
+            }
+            lane_sm.ready_seen = r;
+        }
+        __syncthreads();
+    }
+
+    __device__ void load_row(const double *r, int frame) {
         row = r;
-        if (p.acrow_smem)
+        if (p.ready) {
+            wait_rows(frame + 1);
+            // L2-only loads (ld.cg): a published row was never cached before it was
+            // written (the host aligns chunks to 128-byte lines); ld.cv would be
+            // safe without that but costs ~130 us per frame on mapped memory.
+            for (int d = threadIdx.x; d < p.D; d += blockDim.x) lane_dyn[d] = __dmul_rn(__ldcg(r + d), p.scale);
+        } else if (p.acrow_smem) {
             for (int d = threadIdx.x; d < p.D; d += blockDim.x) lane_dyn[d] = __dmul_rn(__ldg(r + d), p.scale);
+        }
     }
 
     // Clear the counter set of the NEXT frame (its previous readers are done).
@@ -937,6 +963,7 @@ __device__ __forceinline__ void init_smem(unsigned round_ctr) {
         sm.err = sm.err_frame = 0;
         sm.err_aux = 0;
         sm.round_id = round_ctr;
+        sm.ready_seen = 0;
         sm.c_tok = sm.c_scan = sm.c_cand = sm.c_front = sm.c_escan = sm.c_ecand = sm.c_next = 0;
     }
 }
@@ -1035,7 +1062,7 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         if (G.leader()) sm.c_tok += np;
         ln.par = t & 1;
         reset_done = false;
-        ln.load_row(io.costs + (long long)(t - 1) * p.D);
+        ln.load_row(io.costs + (long long)(t - 1) * p.D, t - 1);
         if (g.has_eps) ln.fix_preds((t - 1) & 1, t - 1, tbp, np);
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff, t);
@@ -1337,7 +1364,7 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     double cutoff = cutoff_in;
     ln.par = 1;
     if (mode == 0) {
-        ln.load_row(io.costs);
+        ln.load_row(io.costs, 0);
         __syncthreads();
         const double best = ln.emit(io.tok_state, io.tok_cost, n, p.beam, 1);
         if (!(best < inf_d())) {

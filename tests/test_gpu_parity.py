@@ -231,6 +231,29 @@ def test_device_resident_and_zero_copy_paths_agree(oracle_mod, monkeypatch):
         assert r.alignment == list(zip(il[il > 0].tolist(), range(int((il > 0).sum()))))
 
 
+@pytest.mark.parametrize("D", [2000, 1999])
+def test_progressive_zero_copy_staging(oracle_mod, monkeypatch, D):
+    """Lane-kernel 1-best decodes of host numpy costs stage the rows progressively
+    (frame chunks published through a mapped counter while the kernel runs).
+    Repeated calls through the same staging buffer with new data and ragged
+    lengths, multi-threaded staging (> 8 MB), and the non-progressive path all
+    equal the oracle bit-exactly."""
+    monkeypatch.setenv("LB_MODE", "lane")
+    w = synthetic.hclg_graph(8, num_states=200_000, pool_size=3000, num_pdfs=D)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=1500)
+    for rnd in range(5):
+        mats = [np.ascontiguousarray(synthetic.hclg_matrix(900 + 10 * rnd + i, num_frames=120 + 37 * i + rnd,
+                                                           num_pdfs=D).costs) for i in range(8)]
+        assert sum(m.nbytes for m in mats) > (8 << 20)
+        tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=1500)
+        assert all(st == 0)
+        if rnd == 4:
+            monkeypatch.setenv("LB_NO_PROGRESSIVE", "1")
+        res = lb.decode_batch(w, mats, cfg, want_lattice=False)
+        assert [r.total_cost for r in res] == tc.tolist(), rnd
+    monkeypatch.delenv("LB_NO_PROGRESSIVE")
+
+
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
     """compute-sanitizer finds no memory error, shared-memory race or barrier misuse
