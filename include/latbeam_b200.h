@@ -107,6 +107,12 @@ int lb_result_final_lattice(const lb_result *r, int32_t utt, int64_t *num_nodes,
 int lb_result_final_arrays(const lb_result *r, int32_t utt, uint64_t *node_keys, int64_t *final_ids,
                            double *final_costs, int32_t *from, int32_t *to, int32_t *ilabel,
                            int32_t *olabel, double *graph_cost, double *acoustic_cost);
+/* The same arrays in the FinalLattice dtypes (int64 ids/labels, node keys split
+ * into node_frame / node_idx), widened on all host threads from the pinned D2H
+ * arena.  Any pointer may be NULL to skip that array. */
+int lb_result_final_arrays64(const lb_result *r, int32_t utt, int64_t *node_frame, int64_t *node_idx,
+                             int64_t *final_ids, double *final_costs, int64_t *from, int64_t *to, int64_t *ilabel,
+                             int64_t *olabel, double *graph_cost, double *acoustic_cost);
 /* counters[8]: tokens expanded, arcs scanned, emitting candidates, epsilon
  * frontier entries, epsilon arcs scanned, epsilon candidates, tokens kept,
  * lattice arcs. */

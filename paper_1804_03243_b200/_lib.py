@@ -47,6 +47,7 @@ SIGNATURES = {
     "lb_result_warp_phases": (C.c_int, [PV, PD, PD]),
     "lb_result_free": (None, [PV]),
     "lb_oracle_wer_batch": (C.c_int, [C.c_int32, C.c_int32, PV, P64]),
+    "lb_result_final_arrays64": (C.c_int, [PV, C.c_int32, P64, P64, P64, PD, P64, P64, P64, P64, PD, PD]),
     "lb_lattice_text": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64, P64, PD, C.c_int64, P64, P64, P64,
                                     P64, PD, PD, C.c_char_p, C.c_int64]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,

@@ -48,6 +48,29 @@ cudaError_t dalloc(T **p, size_t n) {
     return cudaMalloc((void **)p, std::max<size_t>(n, 1) * sizeof(T));
 }
 
+// Pinned host arena for final lattice arrays: D2H at full link speed into
+// page-locked memory that is reused across calls (a result keeps the arena it
+// points into alive; the graph reuses it only once no result holds it).
+struct HostArena {
+    char *p = nullptr;
+    size_t cap = 0, used = 0;
+    HostArena() = default;
+    HostArena(const HostArena &) = delete;
+    ~HostArena() {
+        if (p) cudaFreeHost(p);
+    }
+};
+template <class T>
+struct Span {
+    T *p = nullptr;
+    size_t n = 0;
+    T *data() const { return p; }
+    size_t size() const { return n; }
+    T *begin() const { return p; }
+    T *end() const { return p + n; }
+    T &operator[](size_t i) const { return p[i]; }
+};
+
 struct UttHost {
     int status = 0;
     std::string msg, bound;
@@ -63,11 +86,12 @@ struct UttHost {
     // final lattice (device-finalised, lattice.py:500-598)
     bool has_final = false;
     int64_t fl_start = -1;
-    std::vector<uint64_t> fl_nodes;        // (frame << 32) | state-sorted index, ascending
+    std::shared_ptr<HostArena> fl_arena;  // owns the spans below
+    Span<uint64_t> fl_nodes;               // (frame << 32) | state-sorted index, ascending
     std::vector<int64_t> fl_final_ids;
     std::vector<double> fl_final_costs;
-    std::vector<int32_t> fl_from, fl_to, fl_il, fl_ol;
-    std::vector<double> fl_g, fl_ac;
+    Span<int32_t> fl_from, fl_to, fl_il, fl_ol;
+    Span<double> fl_g, fl_ac;
 };
 
 // Growable device scratch of the lattice finaliser.
@@ -160,6 +184,7 @@ struct lb_graph {
     size_t d_costs_cap = 0;
     double *h_stage = nullptr;
     size_t h_stage_cap = 0;
+    std::shared_ptr<HostArena> fl_arena;   // final-lattice D2H arena (see HostArena)
     int *h_ready = nullptr;   // progressive staging counter (mapped pinned)
     int *d_ready = nullptr;
     GraphDev dev() const {
@@ -401,6 +426,27 @@ int validate_cfg(const lb_config *c) {
 }
 
 // Device lattice finalisation of one utterance (lb_lattice.cuh); fills u.fl_*.
+// n elements of T from the graph's pinned arena, kept alive by u.
+template <class T>
+int arena_take(lb_graph *g, UttHost &u, size_t n, Span<T> &out) {
+    const size_t bytes = (n * sizeof(T) + 255) & ~(size_t)255;
+    std::shared_ptr<HostArena> &A = g->fl_arena;
+    if (!A || A->used + bytes > A->cap) {
+        const size_t cap = std::max<size_t>(bytes, A ? 2 * A->cap : ((size_t)64 << 20));
+        if (!A || A.use_count() > 1) A = std::make_shared<HostArena>();   // a result still reads the old one
+        if (A->p) cudaFreeHost(A->p);
+        A->p = nullptr;
+        A->cap = A->used = 0;
+        CK(cudaHostAlloc((void **)&A->p, cap, cudaHostAllocDefault));
+        A->cap = cap;
+    }
+    out.p = reinterpret_cast<T *>(A->p + A->used);
+    out.n = n;
+    A->used += bytes;
+    if (u.fl_arena != A) u.fl_arena = A;
+    return LB_OK;
+}
+
 // Returns LB_OK, or an LB_* status for CUDA failures; reference DecodeFailures
 // (no surviving arc / start not connected / no terminal node) go to u.status.
 int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, double lattice_beam, int partial,
@@ -492,8 +538,13 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
     CK(cudaGetLastError());
     unsigned long long nf = 0;
     CK(cudaMemcpyAsync(&nf, sc.count + 1, 8, cudaMemcpyDeviceToHost, st));
-    u.fl_nodes.resize(nn);
-    u.fl_from.resize(m); u.fl_to.resize(m); u.fl_il.resize(m); u.fl_ol.resize(m); u.fl_g.resize(m); u.fl_ac.resize(m);
+    if (int rc = arena_take(g, u, nn, u.fl_nodes)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_from)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_to)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_il)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_ol)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_g)) return rc;
+    if (int rc = arena_take(g, u, m, u.fl_ac)) return rc;
     CK(cudaMemcpyAsync(u.fl_nodes.data(), sc.nodes0, 8 * (size_t)nn, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(u.fl_from.data(), sc.o_from, 4 * m, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(u.fl_to.data(), sc.o_to, 4 * m, cudaMemcpyDeviceToHost, st));
@@ -691,6 +742,7 @@ int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspa
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
     const bool lat = cfg->want_lattice != 0;
+    if (lat && g->fl_arena && g->fl_arena.use_count() == 1) g->fl_arena->used = 0;   // no result reads it any more
     const bool keep_work = lat && cfg->keep_work_lattice != 0;
     const bool packs = cfg->collect_frame_packs != 0 || keep_work;
     int tmax = 1;
@@ -1364,6 +1416,41 @@ int lb_result_final_arrays(const lb_result *r, int32_t utt, uint64_t *node_keys,
     if (olabel) std::memcpy(olabel, u.fl_ol.data(), 4 * m);
     if (graph_cost) std::memcpy(graph_cost, u.fl_g.data(), 8 * m);
     if (acoustic_cost) std::memcpy(acoustic_cost, u.fl_ac.data(), 8 * m);
+    return LB_OK;
+}
+
+int lb_result_final_arrays64(const lb_result *r, int32_t utt, int64_t *node_frame, int64_t *node_idx,
+                             int64_t *final_ids, double *final_costs, int64_t *from, int64_t *to, int64_t *ilabel,
+                             int64_t *olabel, double *graph_cost, double *acoustic_cost) {
+    UTT_OR_FAIL
+    if (!u.has_final) return set_err(LB_USAGE, "lattice was not requested");
+    const size_t m = u.fl_from.size(), nn = u.fl_nodes.size(), nf = u.fl_final_ids.size();
+    if (final_ids) std::memcpy(final_ids, u.fl_final_ids.data(), 8 * nf);
+    if (final_costs) std::memcpy(final_costs, u.fl_final_costs.data(), 8 * nf);
+    // widen from the pinned arena on all host threads (the copies are page-fault
+    // bound on fresh numpy pages, which parallelise)
+    unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (m + nn < ((size_t)1 << 18)) nth = 1;
+    auto work = [&](unsigned w) {
+        const size_t a0 = m * w / nth, a1 = m * (w + 1) / nth;
+        for (size_t k = a0; k < a1; k++) {
+            if (from) from[k] = u.fl_from[k];
+            if (to) to[k] = u.fl_to[k];
+            if (ilabel) ilabel[k] = u.fl_il[k];
+            if (olabel) olabel[k] = u.fl_ol[k];
+        }
+        if (graph_cost) std::memcpy(graph_cost + a0, u.fl_g.data() + a0, 8 * (a1 - a0));
+        if (acoustic_cost) std::memcpy(acoustic_cost + a0, u.fl_ac.data() + a0, 8 * (a1 - a0));
+        const size_t b0 = nn * w / nth, b1 = nn * (w + 1) / nth;
+        for (size_t k = b0; k < b1; k++) {
+            if (node_frame) node_frame[k] = (int64_t)(u.fl_nodes[k] >> 32);
+            if (node_idx) node_idx[k] = (int64_t)(u.fl_nodes[k] & 0xFFFFFFFFull);
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nth; w++) th.emplace_back(work, w);
+    work(0);
+    for (auto &t : th) t.join();
     return LB_OK;
 }
 

@@ -140,6 +140,27 @@ __device__ __forceinline__ void rst_u128(void *a, ulonglong2 v) {
 #endif
 }
 
+// Read-only graph records (shared by every lane).  LB_GRAPH_HINT: L2 evict_last.
+__device__ __forceinline__ int4 gld4(const int4 *a) {
+#if defined(LB_GRAPH_HINT) && defined(LB_L2HINT)
+    int4 v;
+    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a), "l"(l2_pol()));
+    return v;
+#else
+    return __ldg(a);
+#endif
+}
+__device__ __forceinline__ uint2 gld2(const uint2 *a) {
+#if defined(LB_GRAPH_HINT) && defined(LB_L2HINT)
+    uint2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(l2_pol()));
+    return v;
+#else
+    return __ldg(a);
+#endif
+}
+
 // A winner's {cost, pred, tokidx = -1} in one 16-byte store (the stale token
 // index of an older frame is dead once the frame's emit barrier has passed).
 __device__ __forceinline__ void store_winner(StateRec *r, double cost, int pred) {

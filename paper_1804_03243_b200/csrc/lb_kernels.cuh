@@ -150,7 +150,7 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, in
     }
     for (; base < n; base += step) {
         const bool valid = base + lane < n;
-        const uint2 rg = valid ? __ldg(g.rng + s) : make_uint2(0u, 0u);
+        const uint2 rg = valid ? gld2(g.rng + s) : make_uint2(0u, 0u);
         // prefetch the next group's tokens
         const int nb = base + step;
         unsigned s_n = 0u;
@@ -249,7 +249,11 @@ struct Lane {
 #else
     static constexpr int AUNR = 1;   // touched states per thread per aggregate batch (2 spills at 80 regs)
 #endif
+#ifdef LB_EUNR
+    static constexpr int EUNR = LB_EUNR;
+#else
     static constexpr int EUNR = 2;   // frontier entries per thread per epsilon batch
+#endif
     const GraphDev &g;      // __grid_constant__ kernel parameters: referenced in place,
     const Params &p;        // never copied to local memory
     const LaneWs &L;
@@ -390,7 +394,7 @@ struct Lane {
             int4 r[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++)
-                if (vv[u]) r[u] = __ldg(g.arcs + aa[u]);
+                if (vv[u]) r[u] = gld4(g.arcs + aa[u]);
             unsigned long long known = *(volatile unsigned long long *)run;
             double cand[UNR];
             double bmin = inf_d();
@@ -688,7 +692,7 @@ struct Lane {
 #pragma unroll
                 for (int u = 0; u < EUNR; u++) {
                     if (v[u] == 0xFFFFFFFFu) continue;
-                    er[u] = __ldg(g.erng + v[u]);
+                    er[u] = gld2(g.erng + v[u]);
                     if (r == 0) {
                         c[u] = rld_f64(&rec[v[u]].cost);
                     } else {
@@ -710,7 +714,7 @@ struct Lane {
                     }
                     c_escan += er[u].y - er[u].x;
                     for (unsigned e = er[u].x; e < er[u].y; ++e) {
-                        const int4 rr = __ldg(g.eps + e);
+                        const int4 rr = gld4(g.eps + e);
                         const double cand = __dadd_rn(c[u], __hiloint2double(rr.w, rr.z));
                         if (!(cand <= cutoff)) continue;
                         c_ecand++;

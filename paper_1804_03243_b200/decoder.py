@@ -310,17 +310,14 @@ def _final_lattice(res, u, num_frames) -> FinalLattice:
     nn, st, nf, na = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
     _raise_status(L.lb_result_final_lattice(res, u, C.byref(nn), C.byref(st), C.byref(nf), C.byref(na)),
                   _lib.last_error())
-    keys = np.zeros(nn.value, dtype=np.uint64)
-    fids, fcs = np.zeros(nf.value, dtype=np.int64), np.zeros(nf.value)
-    fr, to, il, ol = (np.zeros(na.value, dtype=np.int32) for _ in range(4))
-    gc, ac = np.zeros(na.value), np.zeros(na.value)
-    _raise_status(L.lb_result_final_arrays(res, u, ptr(keys, PU64), ptr(fids, P64), ptr(fcs, PD),
-                                           ptr(fr, P32), ptr(to, P32), ptr(il, P32), ptr(ol, P32),
-                                           ptr(gc, PD), ptr(ac, PD)), _lib.last_error())
-    k = keys.astype(np.int64)
-    return FinalLattice(int(nn.value), int(st.value), fids, fcs, fr.astype(np.int64),
-                        to.astype(np.int64), il.astype(np.int64), ol.astype(np.int64), gc, ac,
-                        k >> 32, k & 0xFFFFFFFF, num_frames)
+    nfr, nix = np.empty(nn.value, dtype=np.int64), np.empty(nn.value, dtype=np.int64)
+    fids, fcs = np.empty(nf.value, dtype=np.int64), np.empty(nf.value)
+    fr, to, il, ol = (np.empty(na.value, dtype=np.int64) for _ in range(4))
+    gc, ac = np.empty(na.value), np.empty(na.value)
+    _raise_status(L.lb_result_final_arrays64(res, u, ptr(nfr, P64), ptr(nix, P64), ptr(fids, P64), ptr(fcs, PD),
+                                             ptr(fr, P64), ptr(to, P64), ptr(il, P64), ptr(ol, P64),
+                                             ptr(gc, PD), ptr(ac, PD)), _lib.last_error())
+    return FinalLattice(int(nn.value), int(st.value), fids, fcs, fr, to, il, ol, gc, ac, nfr, nix, num_frames)
 
 
 def _attach_lattice(r, wfst, res, u, m, cfg, ntok, nlat, want_lattice, collect_frame_packs):

@@ -16,11 +16,12 @@ for name, n in (("C1", int(sys.argv[1]) if len(sys.argv) > 1 else 4), ("C3", 1))
     cfg = lb.DecodeConfig(beam=d["beam"], lattice_beam=d["lattice_beam"], max_active=d["max_active"],
                           max_lattice_arcs=50_000_000)
     lb.decode_batch(g, mats, cfg)
-    t0 = time.perf_counter()
-    res = lb.decode_batch(g, mats, cfg, collect_timings=True)
-    wall = time.perf_counter() - t0
-    tm = res[0].timings
-    print(f"{name} x{n}: wall {wall:.2f}s  decode {tm['token_passing']:.3f}s prune {tm['lattice_pruning']:.3f}s "
-          f"h2d {tm['h2d']:.3f}s d2h {tm['d2h']:.3f}s  host-rest {wall - tm['token_passing'] - tm['lattice_pruning'] - tm['h2d'] - tm['d2h']:.2f}s  "
-          f"live arcs/utt {np.mean([r.counters['n_lat'] for r in res]):.0f} final arcs/utt {np.mean([r.lattice.num_arcs for r in res]):.0f}",
-          flush=True)
+    for rep in range(3):
+      t0 = time.perf_counter()
+      res = lb.decode_batch(g, mats, cfg, collect_timings=True)
+      wall = time.perf_counter() - t0
+      tm = res[0].timings
+      print(f"{name} x{n}: wall {wall:.2f}s  decode {tm['token_passing']:.3f}s prune {tm['lattice_pruning']:.3f}s "
+            f"h2d {tm['h2d']:.3f}s d2h {tm['d2h']:.3f}s  host-rest {wall - tm['token_passing'] - tm['lattice_pruning'] - tm['h2d'] - tm['d2h']:.2f}s  "
+            f"live arcs/utt {np.mean([r.counters['n_lat'] for r in res]):.0f} final arcs/utt {np.mean([r.lattice.num_arcs for r in res]):.0f}",
+            flush=True)
