@@ -231,6 +231,44 @@ def test_device_resident_and_zero_copy_paths_agree(oracle_mod, monkeypatch):
         assert r.alignment == list(zip(il[il > 0].tolist(), range(int((il > 0).sum()))))
 
 
+def test_results_outlive_later_decodes():
+    """C-ABI results own their final lattices: a result held across later decodes
+    (which reuse the pinned D2H arena once no result points into it) still reads
+    back the lattice it was decoded with."""
+    import ctypes as C
+
+    from paper_1804_03243_b200 import _lib
+    from paper_1804_03243_b200 import decoder as dec
+    w = synthetic.uniform_bench_graph(3, num_states=3000, arcs_per_state=5, num_labels=100)
+    sets = [[np.ascontiguousarray(synthetic.bench_matrix(100 * k + i, num_frames=60, num_labels=100).costs)
+             for i in range(3)] for k in range(3)]
+    cfg = lb.DecodeConfig(beam=10.0, lattice_beam=5.0)
+    want = [lb.decode_batch(w, mats, cfg) for mats in sets]
+    L = _lib.lib()
+    g = dec.device_graph(w, 0)
+
+    def raw(mats):
+        n = len(mats)
+        cptrs = (_lib.PD * n)(*[m.ctypes.data_as(_lib.PD) for m in mats])
+        T = np.asarray([m.shape[0] for m in mats], dtype=np.int32)
+        c = cfg.to_c(True, False)
+        res = _lib.PV()
+        assert L.lb_decode_batch(g.handle, n, cptrs, T.ctypes.data_as(_lib.P32), 100, C.byref(c),
+                                 C.byref(res)) == 0
+        return res
+
+    held = [raw(mats) for mats in sets]          # all three alive at once
+    for k in (1, 0, 2):
+        for u in range(3):
+            assert dec._final_lattice(held[k], u, 60).same_lattice(want[k][u].lattice), (k, u)
+        L.lb_result_free(held[k])
+        held[k] = raw(sets[(k + 1) % 3])         # a decode after a free reuses the arena
+        for u in range(3):
+            assert dec._final_lattice(held[k], u, 60).same_lattice(want[(k + 1) % 3][u].lattice)
+    for r in held:
+        L.lb_result_free(r)
+
+
 @pytest.mark.parametrize("D", [2000, 1999])
 def test_progressive_zero_copy_staging(oracle_mod, monkeypatch, D):
     """Lane-kernel 1-best decodes of host numpy costs stage the rows progressively
