@@ -408,42 +408,45 @@ __global__ void __launch_bounds__(NT, 1) b_epsilon(const __grid_constant__ Graph
             const unsigned v = __ldcg(fs + k);
             const uint2 er = __ldg(g.erng + v);
             double cu;
+            unsigned src = 0;
             if (r == 0) {
-                cu = __ldcg(&rec[v].cost);
+                cu = rld_f64(&rec[v].cost);
             } else {
-                const ulonglong2 w2 = __ldcg(reinterpret_cast<const ulonglong2 *>(rprev + v));
-                __stcg(reinterpret_cast<ulonglong2 *>(rprev + v), make_ulonglong2(~0ull, ~0ull));
+                const ulonglong2 w2 = rld_u128(rprev + v);
+                rst_u128(rprev + v, make_ulonglong2(~0ull, ~0ull));
                 cu = __longlong_as_double((long long)w2.y);
-                const unsigned src = __ldg(g.src + (unsigned)w2.x);
-                store_winner(&rec[v], cu, (int)(src << 1));
+                src = __ldg(g.src + (unsigned)w2.x);   // stored after the offers (see the lane kernel)
             }
-            if (!(cu <= cutoff)) continue;
-            c_front++;
-            if (LAT) {
-                const double m = __ldcg(&rec[v].minsnap);
-                if (cu < m) __stcg(&rec[v].minsnap, cu);
-            }
-            c_escan += er.y - er.x;
-            for (unsigned e = er.x; e < er.y; ++e) {
-                const int4 rr = __ldg(g.eps + e);
-                const double cand = __dadd_rn(cu, __hiloint2double(rr.w, rr.z));
-                if (!(cand <= cutoff)) continue;
-                c_ecand++;
-                const unsigned x = (unsigned)rr.x;
-                const unsigned long long word = pack_word(cand, (unsigned)rr.y);
-                const unsigned long long old = atom_min_u64(&rec[x].pack, word);
-                if (old == SENT) {
-                    const int sl = agg_append(&c.ntouched);
-                    __stcg(L.touched + sl, x);
+            if (cu <= cutoff) {
+                c_front++;
+                if (LAT) {
+                    const double m = rld_f64(&rec[v].minsnap);
+                    if (cu < m) rst_f64(&rec[v].minsnap, cu);
                 }
-                if (old > word) {
-                    epswin_min(rcur + x, word, cand);
-                    if (atom_exch_u32(L.tag + x, round_id) != round_id) {
-                        const int sl = agg_append(nnext);
-                        __stcg(fsn + sl, x);
+                c_escan += er.y - er.x;
+                for (unsigned e = er.x; e < er.y; ++e) {
+                    const int4 rr = __ldg(g.eps + e);
+                    const double cand = __dadd_rn(cu, __hiloint2double(rr.w, rr.z));
+                    if (!(cand <= cutoff)) continue;
+                    c_ecand++;
+                    const unsigned x = (unsigned)rr.x;
+                    const unsigned long long word = pack_word(cand, (unsigned)rr.y);
+                    const unsigned long long old = atom_min_u64(&rec[x].pack, word);
+                    if (old == SENT) {
+                        const int sl = agg_append(&c.ntouched);
+                        __stcg(L.touched + sl, x);
+                    }
+                    if (old > word) {
+                        const unsigned tg = atom_exch_u32(L.tag + x, round_id);
+                        epswin_min(rcur + x, word, cand);
+                        if (tg != round_id) {
+                            const int sl = agg_append(nnext);
+                            __stcg(fsn + sl, x);
+                        }
                     }
                 }
             }
+            if (r > 0) store_winner(&rec[v], cu, (int)(src << 1));
         }
         cl.sync();
     }

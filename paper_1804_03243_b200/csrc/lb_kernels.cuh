@@ -684,6 +684,7 @@ struct Lane {
                 unsigned v[EUNR];
                 uint2 er[EUNR];
                 double c[EUNR];
+                unsigned src[EUNR];
 #pragma unroll
                 for (int u = 0; u < EUNR; u++) {
                     const int k = k0 + u * bd;
@@ -699,8 +700,9 @@ struct Lane {
                         const ulonglong2 w2 = rld_u128(rprev + v[u]);
                         rst_u128(rprev + v[u], make_ulonglong2(~0ull, ~0ull));
                         c[u] = __longlong_as_double((long long)w2.y);
-                        const unsigned src = __ldg(g.src + (unsigned)w2.x);
-                        store_winner(&rec[v[u]], c[u], (int)(src << 1));
+                        // the winner's source state: loaded now, stored after the
+                        // offers below (a store waiting on this load would stall them)
+                        src[u] = __ldg(g.src + (unsigned)w2.x);
                     }
                 }
 #pragma unroll
@@ -726,13 +728,20 @@ struct Lane {
                             __stcg(tl + sl, x);
                         }
                         if (old > word) {
+                            // tag exchange issued before the winner CAS: both in flight together
+                            const unsigned tg = atom_exch_u32(L.tag + x, round_id);
                             epswin_min(rcur + x, word, cand);
-                            if (atom_exch_u32(L.tag + x, round_id) != round_id) {
+                            if (tg != round_id) {
                                 const int sl = agg_append(nnext);
                                 __stcg(fsn + sl, x);
                             }
                         }
                     }
+                }
+                if (r > 0) {
+#pragma unroll
+                    for (int u = 0; u < EUNR; u++)
+                        if (v[u] != 0xFFFFFFFFu) store_winner(&rec[v[u]], c[u], (int)(src[u] << 1));
                 }
             }
             wend(3, t0);
