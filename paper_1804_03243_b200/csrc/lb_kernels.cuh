@@ -242,7 +242,7 @@ struct Lane {
 #ifdef LB_WUNR
     static constexpr int WUNR = LB_WUNR;
 #else
-    static constexpr int WUNR = UNR; // candidates per thread per winners batch
+    static constexpr int WUNR = 1;   // candidates per thread per winners batch (next batch prefetched)
 #endif
 #ifdef LB_AUNR
     static constexpr int AUNR = LB_AUNR;
@@ -544,16 +544,31 @@ struct Lane {
             if (nown == 0xFFFFFFFFu) lane_sm.err_aux = nown;
             if (p.exp & 8) { wend(2, t0); return; }
         }
+        // candidate records of the next batch are fetched one batch ahead
+        int4 en[WUNR];
+        int tn[WUNR];
+#pragma unroll
+        for (int u = 0; u < WUNR; u++) {
+            const int k = warp * 32 * WUNR + u * 32 + lane;
+            en[u].x = -1;
+            tn[u] = 0;
+            if (k < nc) {
+                en[u] = CAND_LD(cb + k);
+                tn[u] = CAND_LD(cbi + k);
+            }
+        }
         for (int kb = warp * 32 * WUNR; kb < nc; kb += nw * 32 * WUNR) {
             int4 e[WUNR];
             int ti[WUNR];
 #pragma unroll
             for (int u = 0; u < WUNR; u++) {
-                const int k = kb + u * 32 + lane;
-                e[u].x = -1;
+                e[u] = en[u];
+                ti[u] = tn[u];
+                const int k = kb + nw * 32 * WUNR + u * 32 + lane;
+                en[u].x = -1;
                 if (k < nc) {
-                    e[u] = CAND_LD(cb + k);
-                    if (e[u].x != -1) ti[u] = CAND_LD(cbi + k);
+                    en[u] = CAND_LD(cb + k);
+                    tn[u] = CAND_LD(cbi + k);
                 }
             }
             unsigned long long pk[WUNR];
@@ -839,12 +854,20 @@ struct Lane {
         TokStage st = tok_stage();
         WStage sf = fix_stage();
         const unsigned long long t0 = wbegin();
+        // touched-list entries of the next batch are fetched one batch ahead
+        unsigned vn[AUNR];
+#pragma unroll
+        for (int u = 0; u < AUNR; u++) {
+            const int k = warp * 32 * AUNR + u * 32 + lane;
+            vn[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
+        }
         for (int kb = warp * 32 * AUNR; kb < nt; kb += nw * 32 * AUNR) {
             unsigned v[AUNR];
 #pragma unroll
             for (int u = 0; u < AUNR; u++) {
-                const int k = kb + u * 32 + lane;
-                v[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
+                v[u] = vn[u];
+                const int k = kb + nw * 32 * AUNR + u * 32 + lane;
+                vn[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
             }
             RecView rv[AUNR];
 #pragma unroll
