@@ -263,7 +263,7 @@ def config_dict(args, note=""):
     d = {"workload": "C4: sequence-parallel batch on the C2 HCLG graph (1-best, beam 13, max-active 7000)",
          "graph": f"hclg_graph(seed=0, states={args.states}), 3000 pdfs, acyclic epsilon depth<=4",
          "utts_per_step_per_gpu": args.utts, "frames_per_utt": args.frames, "beam": 13.0,
-         "max_active": 7000, "lanes": args.lanes or "auto", "threads_per_cta": args.threads or 768,
+         "max_active": 7000, "lanes": args.lanes or "auto", "threads_per_cta": args.threads or 640,
          "ctas_per_lane": args.ctas or 2,
          "l2": "flushed between steps (256 MiB write); graph 0.36 GB > L2"}
     if note:

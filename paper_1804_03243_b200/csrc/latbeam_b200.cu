@@ -419,8 +419,9 @@ int validate_cfg(const lb_config *c) {
     if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
     if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
     if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
-    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 768)
-        return set_err(LB_USAGE, "threads_per_lane must be 512 or 768");
+    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 640 &&
+        c->threads_per_lane != 768)
+        return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
     if (c->ctas_per_lane < 0 || c->ctas_per_lane > 4) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 4]");
     return LB_OK;
 }
@@ -754,7 +755,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     tok_cap = std::min<int64_t>(tok_cap, (int64_t)1 << 31);
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
-    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 768;
+    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 640;
     // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
     // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
     // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
@@ -826,9 +827,12 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     (lat ? (prof ? decode_kernel<NT, U, true, true> : decode_kernel<NT, U, true, false>) \
          : (prof ? decode_kernel<NT, U, false, true> : decode_kernel<NT, U, false, false>))
     KernT kern;
-    if (threads == 768) kern = LB_PICK(768, 2);
+// 640 threads (96 registers, few spills) measured best on C4: 440k vs 392k
+    // frames/s at 768 and 417k at 512 (tools/cta_sweep.sh)
+    if (threads == 640) kern = LB_PICK(640, 2);
+    else if (threads == 768) kern = LB_PICK(768, 2);
     else if (threads == 512) kern = LB_PICK(512, 4);
-    else return set_err(LB_USAGE, "threads_per_lane must be 512 or 768");
+    else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
 #undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();

@@ -44,7 +44,7 @@ class DecodeConfig:
     Added: `max_active` (0 = off, the reference behaviour; histogram cutoff,
     DESIGN.md §3), `token_arena` (tokens kept per utterance over all frames,
     0 = auto), `lanes` (utterances in flight per launch, 0 = auto),
-    `threads_per_lane` (CTA size, 0 = 768), `ctas_per_lane` (thread-block
+    `threads_per_lane` (CTA size 512/640/768, 0 = 640), `ctas_per_lane` (thread-block
     cluster size of a lane, 0 = auto), `device` (CUDA ordinal),
     `keep_work_lattice` (also return `DecodeResult.work_lattice`, every live
     arc with its extra cost; the final lattice is always built on the device).
@@ -86,8 +86,8 @@ class DecodeConfig:
                      "device"):
             if int(getattr(self, name)) < 0:
                 raise UsageError(f"{name} must be >= 0")
-        if int(self.threads_per_lane) not in (0, 512, 768):
-            raise UsageError("threads_per_lane must be 512 or 768")
+        if int(self.threads_per_lane) not in (0, 512, 640, 768):
+            raise UsageError("threads_per_lane must be 512, 640 or 768")
         if not 0 <= int(self.ctas_per_lane) <= 4:
             raise UsageError("ctas_per_lane must be in [0, 4]")
 

@@ -56,12 +56,13 @@ def compare_lattice(got, ref, lattice_beam):
 
 
 def decode_both(w, m, oracle, beam, lattice_beam=4.0, scale=1.0, max_active=0, want_lattice=True,
-                **cfg_kw):
+                device_kw=None, **cfg_kw):
     ref = oracle.decode(w, m, beam, lattice_beam=lattice_beam, acoustic_scale=scale,
                         max_active=max_active, want_lattice=want_lattice, **cfg_kw)
     cfg = lb.DecodeConfig(beam=beam, lattice_beam=lattice_beam, acoustic_scale=scale,
                           max_active=max_active, max_lattice_arcs=50_000_000, keep_work_lattice=True,
-                          **{k: v for k, v in cfg_kw.items() if k in ("max_tokens_per_frame",)})
+                          **{k: v for k, v in cfg_kw.items() if k in ("max_tokens_per_frame",)},
+                          **(device_kw or {}))
     try:
         got = lb.decode_utterance(w, m, cfg, want_lattice=want_lattice, collect_frame_packs=True)
     except lb.LatbeamError as exc:

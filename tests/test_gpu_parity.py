@@ -60,6 +60,20 @@ def test_random_corpus_1best_modes(oracle_mod, monkeypatch, mode, base, cycles, 
         check_pair(got, ref, 4.0, want_lattice=False)
 
 
+@pytest.mark.parametrize("threads", [512, 640, 768])
+def test_lane_cta_sizes(oracle_mod, monkeypatch, threads):
+    """Every supported lane CTA size (kernel template variant) decodes 1-best and
+    lattices bit-exactly vs the oracle, epsilon cycles and max-active included."""
+    monkeypatch.setenv("LB_MODE", "lane")
+    rng = np.random.default_rng(threads)
+    for seed in range(13_000_000, 13_000_025):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=seed % 2 == 0)
+        beam = float(rng.uniform(4.0, 13.0))
+        got, ref = decode_both(w, m, oracle_mod, beam, 3.0, max_active=int(rng.integers(0, 10)),
+                               device_kw={"threads_per_lane": threads})
+        check_pair(got, ref, 3.0)
+
+
 def test_c4_batched_mode_matches_lane_mode(oracle_mod, monkeypatch):
     """The 64-utterance C4 batch in both modes: identical costs and paths."""
     w = synthetic.hclg_graph(2, num_states=400_000, pool_size=6000, num_pdfs=600)
