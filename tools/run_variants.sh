@@ -5,5 +5,5 @@ cd "$(dirname "$0")/.."
 U=$1; T=$2; shift 2
 for name in "$@"; do
   echo "== $name"
-  LB_SO_PATH=build/variants/$name.so timeout 300 python tools/phases.py $U $T 2x768 2>&1 | tail -3
+  LB_SO_PATH=build/variants/$name.so timeout 300 python tools/phases.py $U $T ${CFG:-2x640} 2>&1 | tail -3
 done
