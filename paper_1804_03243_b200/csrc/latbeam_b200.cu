@@ -185,6 +185,8 @@ struct lb_graph {
     double *h_stage = nullptr;
     size_t h_stage_cap = 0;
     std::shared_ptr<HostArena> fl_arena;   // final-lattice D2H arena (see HostArena)
+    size_t fl_taken = 0;                   // arena bytes the current / last lattice decode took
+    size_t fl_expect = 0;                  // growth hint: bytes the rest of this decode will likely take
     int *h_ready = nullptr;   // progressive staging counter (mapped pinned)
     int *d_ready = nullptr;
     GraphDev dev() const {
@@ -433,17 +435,23 @@ int arena_take(lb_graph *g, UttHost &u, size_t n, Span<T> &out) {
     const size_t bytes = (n * sizeof(T) + 255) & ~(size_t)255;
     std::shared_ptr<HostArena> &A = g->fl_arena;
     if (!A || A->used + bytes > A->cap) {
-        const size_t cap = std::max<size_t>(bytes, A ? 2 * A->cap : ((size_t)64 << 20));
+        const size_t cap = std::max<size_t>(std::max<size_t>(bytes, g->fl_expect),
+                                            A ? 2 * A->cap : ((size_t)64 << 20));
         if (!A || A.use_count() > 1) A = std::make_shared<HostArena>();   // a result still reads the old one
         if (A->p) cudaFreeHost(A->p);
         A->p = nullptr;
         A->cap = A->used = 0;
+        const auto ta = std::chrono::steady_clock::now();
         CK(cudaHostAlloc((void **)&A->p, cap, cudaHostAllocDefault));
+        if (getenv("LB_FL_DEBUG"))
+            fprintf(stderr, "[arena] grow %.0f MB in %.1f ms\n", cap / 1e6,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count());
         A->cap = cap;
     }
     out.p = reinterpret_cast<T *>(A->p + A->used);
     out.n = n;
     A->used += bytes;
+    g->fl_taken += bytes;
     if (u.fl_arena != A) u.fl_arena = A;
     return LB_OK;
 }
@@ -451,7 +459,7 @@ int arena_take(lb_graph *g, UttHost &u, size_t n, Span<T> &out) {
 // Returns LB_OK, or an LB_* status for CUDA failures; reference DecodeFailures
 // (no surviving arc / start not connected / no terminal node) go to u.status.
 int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, double lattice_beam, int partial,
-                    FlScratch &sc, cudaStream_t st, UttHost &u) {
+                    FlScratch &sc, cudaStream_t st, UttHost &u, int remaining = 1) {
     long long tb[2], lbase[2];
     CK(cudaMemcpyAsync(&tb[0], d.tok_base + T + 1, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&lbase[0], d.lat_base + T + 1, 8, cudaMemcpyDeviceToHost, st));
@@ -488,11 +496,16 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
     }
     size_t tcap = sc.temp_cap;
     const int nfr = T + 1;
+    // radix sorts run over the key bits actually used
+    auto bits = [](unsigned long long x) { int b = 0; while (x) { b++; x >>= 1; } return std::max(b, 1); };
+    const int sbits = bits((unsigned long long)std::max<int64_t>(g->S - 1, 1));
+    const int fbits = bits((unsigned long long)nfr);
     // 1-2: state-sorted token ranks per frame
-    fl_token_keys<<<nblk, 256, 0, st>>>(d.tok_state, d.tok_base, nfr, ntok, sc.keys0, sc.idx0);
-    CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.keys0, sc.keys1, sc.idx0, sc.idx1, (int)ntok, 0, 64, st));
+    fl_token_keys<<<nblk, 256, 0, st>>>(d.tok_state, d.tok_base, nfr, ntok, sbits, sc.keys0, sc.idx0);
+    CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.keys0, sc.keys1, sc.idx0, sc.idx1, (int)ntok, 0,
+                                       std::min(64, sbits + fbits), st));
     CK(cudaMemsetAsync(sc.start_rank, 0xFF, 8, st));
-    fl_token_rank<<<nblk, 256, 0, st>>>(sc.keys1, sc.idx1, d.tok_base, ntok, g->start, sc.rank, sc.start_rank);
+    fl_token_rank<<<nblk, 256, 0, st>>>(sc.keys1, sc.idx1, d.tok_base, ntok, sbits, g->start, sc.rank, sc.start_rank);
     // 3: survivors
     CK(cudaMemsetAsync(sc.count, 0, 32, st));
     fl_survivors<<<nblk, 256, 0, st>>>(d.lat_extra, nlat, lattice_beam, sc.surv, sc.count);
@@ -511,7 +524,8 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
     fl_arc_fields<<<nblk, 256, 0, st>>>(g->dev(), sc.surv, (long long)m, d.lat_arc, d.lat_from, d.lat_to, d.lat_base,
                                         d.tok_base, nfr, sc.rank, d.costs, D, scale, sc.fk, sc.tk, sc.il, sc.ol, sc.gc,
                                         sc.ac, sc.nodes0);
-    CK(cub::DeviceRadixSort::SortKeys(sc.temp, tcap, sc.nodes0, sc.nodes1, (int)(2 * m), 0, 64, st));
+    CK(cub::DeviceRadixSort::SortKeys(sc.temp, tcap, sc.nodes0, sc.nodes1, (int)(2 * m), 0, std::min(64, 32 + fbits),
+                                      st));
     CK(cub::DeviceSelect::Unique(sc.temp, tcap, sc.nodes1, sc.nodes0, sc.n_unique, (int)(2 * m), st));
     int nn = 0;
     CK(cudaMemcpyAsync(&nn, sc.n_unique, 4, cudaMemcpyDeviceToHost, st));
@@ -526,19 +540,23 @@ int finalize_device(lb_graph *g, const UttDesc &d, int T, int D, double scale, d
             CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.k64a, sc.k64b, pa, pb, (int)m, 0, 64, st));
         } else {
             const unsigned *src = pass == 2 ? sc.ol : pass == 3 ? sc.il : pass == 4 ? sc.tid : sc.fid;
+            const int kb = pass == 3 ? bits((unsigned long long)std::max(g->max_ilabel, 1))
+                         : pass >= 4 ? bits((unsigned long long)std::max(nn - 1, 1)) : 32;
             fl_gather_u32<<<nblk, 256, 0, st>>>(src, pa, (long long)m, sc.k32a);
-            CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.k32a, sc.k32b, pa, pb, (int)m, 0, 32, st));
+            CK(cub::DeviceRadixSort::SortPairs(sc.temp, tcap, sc.k32a, sc.k32b, pa, pb, (int)m, 0, kb, st));
         }
         std::swap(pa, pb);
     }
     fl_emit<<<nblk, 256, 0, st>>>(pa, (long long)m, sc.fid, sc.tid, sc.il, sc.ol, sc.gc, sc.ac, sc.o_from, sc.o_to,
                                   sc.o_il, sc.o_ol, sc.o_g, sc.o_ac);
     // 6: final nodes
-    fl_finals<<<nblk, 256, 0, st>>>(sc.nodes0, nn, T, sc.keys1, d.tok_base, g->fin, partial, sc.fids, sc.fcs,
+    fl_finals<<<nblk, 256, 0, st>>>(sc.nodes0, nn, T, sc.keys1, sbits, d.tok_base, g->fin, partial, sc.fids, sc.fcs,
                                     sc.count + 1);
     CK(cudaGetLastError());
     unsigned long long nf = 0;
     CK(cudaMemcpyAsync(&nf, sc.count + 1, 8, cudaMemcpyDeviceToHost, st));
+    // if the arena must grow, size it for this utterance times the ones left
+    g->fl_expect = ((size_t)8 * nn + (size_t)32 * m + 7 * 256) * (size_t)std::max(remaining, 1) * 5 / 4;
     if (int rc = arena_take(g, u, nn, u.fl_nodes)) return rc;
     if (int rc = arena_take(g, u, m, u.fl_from)) return rc;
     if (int rc = arena_take(g, u, m, u.fl_to)) return rc;
@@ -743,7 +761,29 @@ int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspa
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
     const bool lat = cfg->want_lattice != 0;
-    if (lat && g->fl_arena && g->fl_arena.use_count() == 1) g->fl_arena->used = 0;   // no result reads it any more
+    if (lat) {
+        // size the arena for what the last lattice decode took, so a steady
+        // workload never grows it mid-decode (a growth is a fresh cudaHostAlloc)
+        std::shared_ptr<HostArena> &A = g->fl_arena;
+        const size_t need = g->fl_taken + g->fl_taken / 4;
+        if (g->fl_taken > 0 && (!A || A.use_count() > 1 || A->cap < g->fl_taken)) {
+            if (A && A.use_count() == 1 && A->p) {
+                cudaFreeHost(A->p);
+                A->p = nullptr;
+                A->cap = A->used = 0;
+            } else {
+                A = std::make_shared<HostArena>();
+            }
+            const auto ta = std::chrono::steady_clock::now();
+            CK(cudaHostAlloc((void **)&A->p, need, cudaHostAllocDefault));
+            if (getenv("LB_FL_DEBUG"))
+                fprintf(stderr, "[arena] presize %.0f MB in %.1f ms\n", need / 1e6,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count());
+            A->cap = need;
+        }
+        if (A && A.use_count() == 1) A->used = 0;   // no result reads it any more
+        g->fl_taken = 0;
+    }
     const bool keep_work = lat && cfg->keep_work_lattice != 0;
     const bool packs = cfg->collect_frame_packs != 0 || keep_work;
     int tmax = 1;
@@ -920,7 +960,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             u.path.assign(hpath.begin() + (size_t)path_cap * l, hpath.begin() + (size_t)path_cap * l + plen);
             if (lat) {
                 rc = finalize_device(g, desc[l], T[w0 + l], D, cfg->acoustic_scale, cfg->lattice_beam, u.partial, fl,
-                                     st, u);
+                                     st, u, n - (w0 + l));
                 if (rc) return rc;
             }
             if (packs || keep_work) {

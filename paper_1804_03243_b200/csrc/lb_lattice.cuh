@@ -31,22 +31,25 @@ __device__ __forceinline__ int upper_frame(const long long *base, int nb, long l
     return lo;
 }
 
+// token key = (frame << sbits) | state, sbits = bits of the largest state id, so
+// the radix sort runs over sbits + frame bits only
 __global__ void fl_token_keys(const unsigned *tok_state, const long long *tok_base, int nframes, long long ntok,
-                              unsigned long long *keys, int *idx) {
+                              int sbits, unsigned long long *keys, int *idx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ntok; i += (long long)gridDim.x * blockDim.x) {
         const int f = upper_frame(tok_base, nframes + 1, i);
-        keys[i] = ((unsigned long long)f << 32) | tok_state[i];
+        keys[i] = ((unsigned long long)f << sbits) | tok_state[i];
         idx[i] = (int)i;
     }
 }
 
 __global__ void fl_token_rank(const unsigned long long *skeys, const int *sidx, const long long *tok_base, long long ntok,
-                              int start_state, int *rank, long long *start_rank) {
+                              int sbits, int start_state, int *rank, long long *start_rank) {
+    const unsigned long long smask = (1ull << sbits) - 1ull;
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < ntok; j += (long long)gridDim.x * blockDim.x) {
-        const int f = (int)(skeys[j] >> 32);
+        const int f = (int)(skeys[j] >> sbits);
         const int r = (int)(j - tok_base[f]);
         rank[sidx[j]] = r;
-        if (f == 0 && (int)(unsigned)skeys[j] == start_state) *start_rank = r;
+        if (f == 0 && (int)(skeys[j] & smask) == start_state) *start_rank = r;
     }
 }
 
@@ -132,13 +135,13 @@ __global__ void fl_emit(const int *perm, long long m, const unsigned *fid, const
 }
 
 // final nodes: last-frame nodes (frame == T) with finite graph final cost of their state
-__global__ void fl_finals(const unsigned long long *nodes, int nn, int T, const unsigned long long *skeys,
+__global__ void fl_finals(const unsigned long long *nodes, int nn, int T, const unsigned long long *skeys, int sbits,
                           const long long *tok_base, const double *fin, int partial, long long *ids, double *fcs,
                           unsigned long long *count) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
         if ((int)(nodes[i] >> 32) != T) continue;
         const unsigned idx = (unsigned)nodes[i];
-        const unsigned state = (unsigned)skeys[tok_base[T] + idx];
+        const unsigned state = (unsigned)(skeys[tok_base[T] + idx] & ((1ull << sbits) - 1ull));
         const double fc = partial ? 0.0 : fin[state];
         if (partial || fc < __longlong_as_double(0x7FF0000000000000ll)) {
             const unsigned long long k = atomicAdd(count, 1ull);

@@ -16,7 +16,7 @@ for name, n in (("C1", int(sys.argv[1]) if len(sys.argv) > 1 else 4), ("C3", 1))
     cfg = lb.DecodeConfig(beam=d["beam"], lattice_beam=d["lattice_beam"], max_active=d["max_active"],
                           max_lattice_arcs=50_000_000)
     lb.decode_batch(g, mats, cfg)
-    for rep in range(3):
+    for rep in range(int(os.environ.get("REPS", "3"))):
       t0 = time.perf_counter()
       res = lb.decode_batch(g, mats, cfg, collect_timings=True)
       wall = time.perf_counter() - t0
