@@ -1,8 +1,10 @@
 #!/bin/bash
-# CTA size / emit batch width sweep of the lane kernel (build/variants/extra.so, -DLB_EXTRA)
+# Lane CTA-size sweep of the decode kernel on the C4 shape (run under gpurun).
+# The in-tree build carries the 512/640/768-thread variants; the wider sweep in
+# DESIGN.md §10 (384..768 threads, UNR 1..4) used extra template instantiations
+# that were removed after 640 won.
+# usage: tools/cta_sweep.sh [U] [T]
 cd "$(dirname "$0")/.."
-export LB_SO_PATH=build/variants/extra.so
-for spec in ${SPECS:-768:2 704:2 672:2 640:1 640:2 608:2 576:2 576:3}; do
-  t=${spec%%:*}; u=${spec##*:}
-  echo "threads=$t unr=$u: $(LB_UNR=$u timeout 300 python tools/phases.py ${1:-64} ${2:-100} 2x$t 2>&1 | head -1)"
+for t in ${THREADS:-768 640 512}; do
+  echo "threads=$t: $(timeout 300 python tools/phases.py ${1:-64} ${2:-100} 2x$t 2>&1 | head -1)"
 done
