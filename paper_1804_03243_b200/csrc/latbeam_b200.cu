@@ -799,9 +799,9 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
     // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
     // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
-    // 32: 310k vs 225k; 56: 372k vs 357k); the persistent-lane kernel wins from
-    // ~60 concurrent utterances up (64: 388k vs 375k frames/s; C2 graph,
-    // measured).  LB_MODE=lane|batched overrides.
+    // 32: 317k vs 259k; 40: 341k vs 316k); the persistent-lane kernel wins from
+    // ~44 concurrent utterances up (48: 369k vs 356k; 64: 447k vs 375k frames/s;
+    // C2 graph, tools/mode_crossover.sh).  LB_MODE=lane|batched overrides.
     const char *mode_env = getenv("LB_MODE");
     bool batched = n <= BATCHED_MAX_UTTS;
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;

@@ -58,7 +58,7 @@ constexpr int BUNR = 2;            // arcs per thread per emit batch
 constexpr int BWUNR = 4;           // candidates per thread per winners batch
 constexpr int BAUNR = 2;           // touched states per thread per aggregate batch
 constexpr int BCCH = 256;          // candidate chunk per warp
-constexpr int BATCHED_MAX_UTTS = 60;   // host: batched mode up to this many utterances per call
+constexpr int BATCHED_MAX_UTTS = 44;   // host: batched mode up to this many utterances per call
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(32) b_init(const GraphDev g, const Params p, const LaneWs *lanes,
