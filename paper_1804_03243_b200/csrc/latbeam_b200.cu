@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -186,6 +187,7 @@ struct lb_graph {
     size_t h_stage_cap = 0;
     std::shared_ptr<HostArena> fl_arena;   // final-lattice D2H arena (see HostArena)
     size_t fl_taken = 0;                   // arena bytes the current / last lattice decode took
+    std::map<long long, int> cluster_fit;  // max co-resident lane clusters by (C, threads, smem)
     size_t fl_expect = 0;                  // growth hint: bytes the rest of this decode will likely take
     int *h_ready = nullptr;   // progressive staging counter (mapped pinned)
     int *d_ready = nullptr;
@@ -424,7 +426,7 @@ int validate_cfg(const lb_config *c) {
     if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 640 &&
         c->threads_per_lane != 768)
         return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
-    if (c->ctas_per_lane < 0 || c->ctas_per_lane > 4) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 4]");
+    if (c->ctas_per_lane < 0 || c->ctas_per_lane > 8) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 8]");
     return LB_OK;
 }
 
@@ -758,6 +760,37 @@ int launch_batched_seq(lb_graph *g, const GraphDev &gd, const Params &p, Workspa
     return LB_OK;
 }
 
+// How many C-CTA lane clusters of `threads` threads fit on the device at once
+// (cudaOccupancyMaxActiveClusters on the 1-best lane kernel), cached per graph.
+int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
+    const long long key = ((long long)C << 40) | ((long long)threads << 24) | (long long)dsm;
+    auto it = g->cluster_fit.find(key);
+    if (it != g->cluster_fit.end()) return it->second;
+    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, int);
+    KernT k = threads == 512 ? (KernT)decode_kernel<512, 4, false, false>
+            : threads == 768 ? (KernT)decode_kernel<768, 2, false, false> : (KernT)decode_kernel<640, 2, false, false>;
+    int num = 0;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1)) ==
+            cudaSuccess &&
+        (C <= 8 || cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(C * std::max(1, g->sms / C)));
+        lc.blockDim = dim3((unsigned)threads);
+        lc.dynamicSmemBytes = dsm;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&num, (void *)k, &lc) != cudaSuccess) num = 0;
+    }
+    cudaGetLastError();
+    g->cluster_fit[key] = num;
+    return num;
+}
+
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
     const bool lat = cfg->want_lattice != 0;
@@ -806,7 +839,26 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     bool batched = n <= BATCHED_MAX_UTTS;
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;
     if (mode_env && !strcmp(mode_env, "batched")) batched = true;
-    const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : 2);
+    int autoC = 2;
+    // Small 1-best batches: wider lanes (8- or 4-CTA clusters) beat the batched
+    // mode once every lane's cluster is co-resident (C2 graph, 1-best: 8 utts
+    // 123k vs 113k frames/s at C=8; 24: 291k vs 269k and 32: 370k vs 320k at C=4;
+    // 1-4 utts stay batched).  Lattice decodes keep the measured C=2 / batched rule.
+    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && batched && n > 0) {
+        const size_t dsm = lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX);
+        if (n >= 5 && n <= max_coresident_clusters(g, 8, threads, dsm)) {
+            batched = false;
+            autoC = 8;
+        } else if (n >= 17 && n <= 32 && n <= max_coresident_clusters(g, 4, threads, dsm)) {
+            batched = false;
+            autoC = 4;
+        }
+    }
+    const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
+    if (getenv("LB_MODE_DEBUG"))
+        fprintf(stderr, "[mode] n=%d %s C=%d (fit C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
+                max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
+                max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
     const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
     int lanes_guess = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / 2));
     lanes_guess = std::max(1, std::min(lanes_guess, n > 0 ? n : 1));

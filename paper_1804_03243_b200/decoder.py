@@ -88,8 +88,8 @@ class DecodeConfig:
                 raise UsageError(f"{name} must be >= 0")
         if int(self.threads_per_lane) not in (0, 512, 640, 768):
             raise UsageError("threads_per_lane must be 512, 640 or 768")
-        if not 0 <= int(self.ctas_per_lane) <= 4:
-            raise UsageError("ctas_per_lane must be in [0, 4]")
+        if not 0 <= int(self.ctas_per_lane) <= 8:
+            raise UsageError("ctas_per_lane must be in [0, 8]")
 
     def to_c(self, want_lattice: bool, collect_frame_packs: bool) -> LbConfig:
         return LbConfig(float(self.beam), float(self.lattice_beam), float(self.acoustic_scale),

@@ -74,6 +74,35 @@ def test_lane_cta_sizes(oracle_mod, monkeypatch, threads):
         check_pair(got, ref, 3.0)
 
 
+@pytest.mark.parametrize("ctas", [4, 8])
+def test_wide_lane_clusters(oracle_mod, monkeypatch, ctas):
+    """4- and 8-CTA lane clusters (picked automatically for 5-32 utterance 1-best
+    batches) decode 1-best and lattices bit-exactly vs the oracle."""
+    monkeypatch.setenv("LB_MODE", "lane")
+    rng = np.random.default_rng(ctas)
+    for seed in range(14_000_000, 14_000_020):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=seed % 2 == 1)
+        beam = float(rng.uniform(4.0, 13.0))
+        got, ref = decode_both(w, m, oracle_mod, beam, 3.0, max_active=int(rng.integers(0, 10)),
+                               device_kw={"ctas_per_lane": ctas})
+        check_pair(got, ref, 3.0)
+
+
+@pytest.mark.parametrize("n", [8, 20, 33])
+def test_auto_mode_batches(oracle_mod, n):
+    """The automatic mode choice (8-CTA lanes at 8, 4-CTA lanes at 20, batched at
+    33 utterances) gives the oracle's costs and work counters."""
+    w = synthetic.hclg_graph(4, num_states=300_000, pool_size=4000, num_pdfs=500)
+    mats = [synthetic.hclg_matrix(700 + i, num_frames=30 + (i % 7), num_pdfs=500) for i in range(n)]
+    cfg = lb.DecodeConfig(beam=12.0, max_active=2000)
+    res = lb.decode_batch(w, mats, cfg, want_lattice=False)
+    tc, st, cnt = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=2000)
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()
+    assert [[r.counters["n_tokens"], r.counters["n_scan"], r.counters["n_next"]] for r in res] == \
+        [[c[0], c[1], c[6]] for c in cnt]
+
+
 def test_c4_batched_mode_matches_lane_mode(oracle_mod, monkeypatch):
     """The 64-utterance C4 batch in both modes: identical costs and paths."""
     w = synthetic.hclg_graph(2, num_states=400_000, pool_size=6000, num_pdfs=600)
