@@ -840,23 +840,26 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     if (mode_env && !strcmp(mode_env, "lane")) batched = false;
     if (mode_env && !strcmp(mode_env, "batched")) batched = true;
     int autoC = 2;
-    // Small 1-best batches: wider lanes (8- or 4-CTA clusters) beat the batched
-    // mode once every lane's cluster is co-resident (C2 graph, 1-best: 8 utts
-    // 123k vs 113k frames/s at C=8; 24: 291k vs 269k and 32: 370k vs 320k at C=4;
-    // 1-4 utts stay batched).  Lattice decodes keep the measured C=2 / batched rule.
-    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && batched && n > 0) {
+    // 1-best batches of 5+ utterances: the widest lane cluster (8, 4 or 3 CTAs)
+    // of which n are co-resident beats both the batched mode and 2-CTA lanes
+    // (C2 graph, frames/s: 8 utts 124k vs 112k batched at C=8; 32: 373k vs 317k
+    // at C=4; 44: 415k vs 349k batched and 350k at C=2 with C=3; measured with
+    // tools/mode_auto.sh).  1-4 utterances stay batched; lattice decodes keep the
+    // batched / 2-CTA rule.
+    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= 5) {
         const size_t dsm = lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX);
-        if (n >= 5 && n <= max_coresident_clusters(g, 8, threads, dsm)) {
-            batched = false;
-            autoC = 8;
-        } else if (n >= 17 && n <= 32 && n <= max_coresident_clusters(g, 4, threads, dsm)) {
-            batched = false;
-            autoC = 4;
+        for (int c : {8, 4, 3}) {
+            if (n <= max_coresident_clusters(g, c, threads, dsm)) {
+                batched = false;
+                autoC = c;
+                break;
+            }
         }
     }
     const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
     if (getenv("LB_MODE_DEBUG"))
-        fprintf(stderr, "[mode] n=%d %s C=%d (fit C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
+        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
+                max_coresident_clusters(g, 3, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
                 max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
                 max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
     const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
