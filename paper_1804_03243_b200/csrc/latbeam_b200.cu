@@ -791,6 +791,46 @@ int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
     return num;
 }
 
+// Mode and lane cluster size of a decode call (shared by decode_impl and the
+// staging decision of lb_decode_batch).
+void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched, int &C) {
+    const bool lat = cfg->want_lattice != 0;
+    const int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 640;
+    // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
+    // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
+    // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
+    // 32: 317k vs 259k; 40: 341k vs 316k); the persistent-lane kernel wins from
+    // ~44 concurrent utterances up (48: 369k vs 356k; 64: 447k vs 375k frames/s;
+    // C2 graph, tools/mode_crossover.sh).  LB_MODE=lane|batched overrides.
+    const char *mode_env = getenv("LB_MODE");
+    batched = n <= BATCHED_MAX_UTTS;
+    if (mode_env && !strcmp(mode_env, "lane")) batched = false;
+    if (mode_env && !strcmp(mode_env, "batched")) batched = true;
+    int autoC = 2;
+    // 1-best batches of 5+ utterances: the widest lane cluster (8, 4 or 3 CTAs)
+    // of which n are co-resident beats both the batched mode and 2-CTA lanes
+    // (C2 graph, frames/s: 8 utts 124k vs 112k batched at C=8; 32: 373k vs 317k
+    // at C=4; 44: 415k vs 349k batched and 350k at C=2 with C=3; measured with
+    // tools/mode_auto.sh).  1-4 utterances stay batched; lattice decodes keep the
+    // batched / 2-CTA rule.
+    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= 5) {
+        const size_t dsm = lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX);
+        for (int c : {8, 4, 3}) {
+            if (n <= max_coresident_clusters(g, c, threads, dsm)) {
+                batched = false;
+                autoC = c;
+                break;
+            }
+        }
+    }
+    C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
+    if (getenv("LB_MODE_DEBUG"))
+        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
+                max_coresident_clusters(g, 3, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
+                max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
+                max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
+}
+
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
     const bool lat = cfg->want_lattice != 0;
@@ -829,39 +869,9 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
     int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 640;
-    // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
-    // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
-    // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
-    // 32: 317k vs 259k; 40: 341k vs 316k); the persistent-lane kernel wins from
-    // ~44 concurrent utterances up (48: 369k vs 356k; 64: 447k vs 375k frames/s;
-    // C2 graph, tools/mode_crossover.sh).  LB_MODE=lane|batched overrides.
-    const char *mode_env = getenv("LB_MODE");
-    bool batched = n <= BATCHED_MAX_UTTS;
-    if (mode_env && !strcmp(mode_env, "lane")) batched = false;
-    if (mode_env && !strcmp(mode_env, "batched")) batched = true;
-    int autoC = 2;
-    // 1-best batches of 5+ utterances: the widest lane cluster (8, 4 or 3 CTAs)
-    // of which n are co-resident beats both the batched mode and 2-CTA lanes
-    // (C2 graph, frames/s: 8 utts 124k vs 112k batched at C=8; 32: 373k vs 317k
-    // at C=4; 44: 415k vs 349k batched and 350k at C=2 with C=3; measured with
-    // tools/mode_auto.sh).  1-4 utterances stay batched; lattice decodes keep the
-    // batched / 2-CTA rule.
-    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= 5) {
-        const size_t dsm = lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX);
-        for (int c : {8, 4, 3}) {
-            if (n <= max_coresident_clusters(g, c, threads, dsm)) {
-                batched = false;
-                autoC = c;
-                break;
-            }
-        }
-    }
-    const int C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
-    if (getenv("LB_MODE_DEBUG"))
-        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
-                max_coresident_clusters(g, 3, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
-                max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
-                max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
+    bool batched;
+    int C;
+    choose_mode(g, n, D, cfg, batched, C);
     const int64_t max_tok = std::min<int64_t>(S, cfg->max_tokens_per_frame);
     int lanes_guess = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / 2));
     lanes_guess = std::max(1, std::min(lanes_guess, n > 0 ? n : 1));
@@ -1287,9 +1297,10 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     // kernel reads the mapped staging buffer directly (zero-copy).  Lattice decodes
     // re-read rows in the prune pass, and the batched mode gathers acoustic costs
     // per candidate: those copy the rows to HBM.
-    const char *mode_env = getenv("LB_MODE");
-    const bool lane_mode = cfg->want_lattice || (mode_env && !strcmp(mode_env, "lane")) ||
-                           (n > BATCHED_MAX_UTTS && !(mode_env && !strcmp(mode_env, "batched")));
+    bool batched_mode = true;
+    int lane_c = 1;
+    choose_mode(g, n, D, cfg, batched_mode, lane_c);
+    const bool lane_mode = !batched_mode;
     const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
                            !getenv("LB_E2E_COPY");
     // Stage the caller's matrices into pinned, device-mapped memory with all host
