@@ -338,7 +338,10 @@ def test_progressive_zero_copy_staging(oracle_mod, monkeypatch, D):
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
     """compute-sanitizer finds no memory error, shared-memory race or barrier misuse
-    in a small 1-best + lattice decode with epsilon arcs and max-active."""
+    in small 1-best + lattice decodes with epsilon arcs and max-active:
+    the batched mode and, except under racecheck (over 20 minutes on the lane
+    kernels' shared memory), 8-CTA lanes reading progressively staged host rows and
+    2-CTA lanes with lattices."""
     import os
     import shutil
     import subprocess
@@ -356,7 +359,13 @@ def test_compute_sanitizer_clean(tool):
         "r = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, lattice_beam=3.0, max_active=300))\n"
         "q = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300), want_lattice=False)\n"
         "assert [x.total_cost for x in r] == [x.total_cost for x in q]\n"
-        "print('ok', [x.total_cost for x in r])\n" % root)
+        "if %r:\n"
+        "    m6 = [synthetic.hclg_matrix(30 + i, num_frames=5, num_pdfs=100) for i in range(6)]\n"
+        "    q6 = lb.decode_batch(w, m6, lb.DecodeConfig(beam=10.0, max_active=300), want_lattice=False)\n"
+        "    import os; os.environ['LB_MODE'] = 'lane'\n"
+        "    l6 = lb.decode_batch(w, m6, lb.DecodeConfig(beam=10.0, lattice_beam=3.0, max_active=300))\n"
+        "    assert [x.total_cost for x in q6] == [x.total_cost for x in l6]\n"
+        "print('ok', [x.total_cost for x in r])\n" % (root, tool != "racecheck"))
     res = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable, "-c", prog],
                          capture_output=True, text=True, timeout=1200)
     out = res.stdout + res.stderr
