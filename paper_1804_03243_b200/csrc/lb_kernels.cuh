@@ -321,10 +321,12 @@ struct Lane {
 
     // Frame rows staged progressively by the host (lb_decode_batch, zero-copy):
     // wait until the rows of frames < need are published.  The smem copy of the
-    // flag is only written between barriers, so the test is CTA-uniform and a
-    // barrier is spent only when the staging is behind (about once per chunk).
+    // flag is written only between two barriers (every thread has tested it
+    // before thread 0 updates it), so the test is CTA-uniform; the barriers are
+    // spent only when the copy is behind (about once per chunk).
     __device__ void wait_rows(int need) {
         if (lane_sm.ready_seen >= need) return;
+        __syncthreads();
         if (threadIdx.x == 0) {
             int r;
             for (;;) {
@@ -671,7 +673,8 @@ struct Lane {
     __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
         StateRec *rec = L.rec;
-        unsigned round_id = lane_sm.round_id;
+        const unsigned round_id0 = lane_sm.round_id;
+        unsigned round_id = round_id0;
         unsigned c_escan = 0, c_ecand = 0, c_front = 0;
         unsigned *tl = touched();
         int *ntouched = &lane_sm.ntouched[par];
@@ -770,7 +773,9 @@ struct Lane {
             atomicAdd(&lane_sm.c_ecand, (unsigned long long)c_ecand);
             atomicAdd(&lane_sm.c_front, (unsigned long long)c_front);
         }
-        if (threadIdx.x == 0) lane_sm.round_id = round_id;
+        // (unchanged when no round ran: then no barrier separates this from the
+        // read at the top, so only a changed value is written)
+        if (threadIdx.x == 0 && round_id != round_id0) lane_sm.round_id = round_id;
         if (!ok) G.sync();
         return ok;
     }

@@ -335,6 +335,27 @@ def test_progressive_zero_copy_staging(oracle_mod, monkeypatch, D):
     monkeypatch.delenv("LB_NO_PROGRESSIVE")
 
 
+@pytest.mark.parametrize("ctas", [2, 8])
+def test_racecheck_lane_kernel(ctas):
+    """racecheck finds no shared-memory hazard in the persistent-lane kernel
+    (tiny 1-best with progressive staging, and lattice decodes; 2- and 8-CTA
+    clusters).  It caught a barrier-divergence race in the staging wait."""
+    import os
+    import shutil
+    import subprocess
+    import sys
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([cs, "--tool", "racecheck", "--error-exitcode", "9", sys.executable,
+                          os.path.join(root, "tools", "racecheck_lane.py"), str(ctas)],
+                         capture_output=True, text=True, timeout=900)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-6000:]
+    assert "ok %d" % ctas in res.stdout and "RACECHECK SUMMARY: 0 hazards displayed (0 errors" in out, out[-3000:]
+
+
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
     """compute-sanitizer finds no memory error, shared-memory race or barrier misuse
