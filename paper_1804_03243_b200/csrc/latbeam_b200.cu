@@ -1309,9 +1309,14 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     // through a mapped counter the lanes wait on (Params::ready), so the copy
     // overlaps the decode instead of preceding it.
     const size_t bytes = total * 8;
-    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    if (bytes < ((size_t)8 << 20)) nth = 1;
     const bool progressive = zero_copy && !getenv("LB_NO_PROGRESSIVE") && n > 0;
+    // A blocking copy uses every host thread.  A progressive one needs only to
+    // stay ahead of the decode (~11 GB/s at C4), and at full width it competes
+    // with the lanes' zero-copy reads for host memory: 4 threads measured best
+    // (C4 e2e 391k vs 368k frames/s with 16; tools/e2e_time.py).
+    unsigned nth = std::max(1u, std::min(progressive ? 4u : 32u, std::thread::hardware_concurrency()));
+    if (const char *se = getenv("LB_STAGE_THREADS")) nth = std::max(1, atoi(se));
+    if (bytes < ((size_t)8 << 20)) nth = 1;
     int tmax = 1;
     for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
     // Frames per published chunk.  16 rows of D doubles are 128*D bytes, so with

@@ -18,7 +18,7 @@ mats = [np.ascontiguousarray(synthetic.hclg_matrix(100 + i, num_frames=T).costs)
 cfg = lb.DecodeConfig(beam=13.0, max_active=7000)
 print("cpus", os.cpu_count(), flush=True)
 VARIANTS = {"progressive": {}, "no_progressive": {"LB_NO_PROGRESSIVE": "1"}, "copy": {"LB_E2E_COPY": "1"},
-            "prog_ldg": {"LB_EXP": "64"}, "prog_ldcg": {"LB_EXP": "128"}}
+            "st2": {"LB_STAGE_THREADS": "2"}, "st4": {"LB_STAGE_THREADS": "4"}, "st8": {"LB_STAGE_THREADS": "8"}}
 names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["progressive", "no_progressive", "copy"]
 for name in names:
     env = VARIANTS[name]
