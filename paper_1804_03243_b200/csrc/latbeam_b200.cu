@@ -174,7 +174,8 @@ struct lb_graph {
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
     std::mutex mu;
-    Workspace ws;
+    Workspace ws;    // decode lanes
+    Workspace ws1;   // the single-op surfaces (expand_*): one small lane, never evicts ws
     // batched mode: captured CUDA graph of one wave's launch sequence, reused
     // while (workspace, lanes, frames, blocks per lane, Params) stay the same
     cudaGraphExec_t bexec = nullptr;
@@ -221,9 +222,8 @@ struct lb_result {
 
 namespace {
 
-int ensure_workspace(lb_graph *g, int lanes, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap, int path_cap,
-                     int tmax, bool packs, bool lat) {
-    Workspace &w = g->ws;
+int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap,
+                     int path_cap, int tmax, bool packs, bool lat) {
     if (w.lanes >= lanes && w.C == C && w.S == g->S && w.ccap >= ccap && w.tok_cap >= tok_cap &&
         w.lat_cap >= lat_cap && w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat))
         return LB_OK;
@@ -303,6 +303,24 @@ int ensure_workspace(lb_graph *g, int lanes, int C, int64_t ccap, int64_t tok_ca
     w.tmax = tmax;
     w.packs = packs;
     w.lat = lat;
+    return LB_OK;
+}
+
+// Epsilon round tags (LaneWs::tag) are compared against a 32-bit per-lane round
+// counter that persists across decodes.  Once any lane's counter passes 2^31,
+// reset every tag and counter of the workspace, long before a wrap could make a
+// stale tag equal the current round (one decode uses far fewer than 2^31 rounds).
+int guard_round_tags(Workspace &w, cudaStream_t st) {
+    if (w.lanes <= 0) return LB_OK;
+    std::vector<unsigned> rc(w.lanes);
+    CK(cudaMemcpyAsync(rc.data(), w.round_ctr, 4 * (size_t)w.lanes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    unsigned mx = 0;
+    for (unsigned x : rc) mx = std::max(mx, x);
+    if (mx < 0x80000000u && !getenv("LB_FORCE_TAG_RESET")) return LB_OK;
+    CK(cudaMemsetAsync(w.tag, 0, (size_t)w.S * w.lanes * 4, st));
+    CK(cudaMemsetAsync(w.round_ctr, 0, (size_t)w.lanes * 4, st));
+    CK(cudaStreamSynchronize(st));
     return LB_OK;
 }
 
@@ -890,18 +908,21 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     if (!fits) {   // size the lane count to the device memory left (the workspace is reused across calls)
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        const size_t reuse = w0.C == C ? (size_t)w0.lanes * lane_bytes(S, C, w0.ccap, w0.tok_cap, w0.lat_cap,
-                                                                        w0.path_cap, w0.tmax, w0.packs, w0.lat) : 0;
+        // the current workspace is freed before the new one is allocated, whatever its shape
+        const size_t reuse = w0.lanes > 0 ? (size_t)w0.lanes * lane_bytes(S, w0.C, w0.ccap, w0.tok_cap, w0.lat_cap,
+                                                                           w0.path_cap, w0.tmax, w0.packs, w0.lat)
+                                          : 0;
         const size_t budget = (size_t)((double)(free_b + reuse) * 0.85);
         while (lanes > 1 && (size_t)lanes * per_lane > budget) lanes--;
         if ((size_t)lanes * per_lane > budget)
             return set_err(LB_CAPACITY, "not enough device memory for one decode lane; lower token_arena / max_lattice_arcs");
     }
-    int rc = ensure_workspace(g, lanes, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    int rc = ensure_workspace(g, g->ws, lanes, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
     if (rc) return rc;
     Workspace &w = g->ws;
 
     Params p;
+    std::memset(&p, 0, sizeof(p));   // padding too: the batched-mode graph cache keys on the raw bytes
     p.beam = cfg->beam;
     p.lattice_beam = cfg->lattice_beam;
     p.scale = cfg->acoustic_scale;
@@ -954,7 +975,10 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     std::vector<int> hi(8 * lanes);
     std::vector<double> hd(4 * lanes);
     std::vector<long long> hc(8 * lanes);
-    std::vector<int> hpath((size_t)path_cap * lanes);
+    // best paths are laid out at the workspace's stride (slot_desc), which can be
+    // larger than this call's path_cap when an earlier call grew the workspace
+    const size_t pstride = (size_t)w.path_cap;
+    std::vector<int> hpath(pstride * lanes);
     for (int w0 = 0; w0 < n; w0 += lanes) {
         const int nw = std::min(lanes, n - w0);
         for (int l = 0; l < nw; l++) desc[l] = slot_desc(w, l, dev_costs[w0 + l], T[w0 + l], tok_cap, lat_cap);
@@ -1002,7 +1026,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaMemcpyAsync(hi.data(), w.out_i, 8 * sizeof(int) * nw, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hd.data(), w.out_d, 4 * sizeof(double) * nw, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hc.data(), w.out_c, 8 * sizeof(long long) * nw, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hpath.data(), w.path, sizeof(int) * (size_t)path_cap * nw, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hpath.data(), w.path, sizeof(int) * pstride * nw, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -1022,7 +1046,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             u.partial = hi[8 * l + 2];
             u.total_cost = hd[4 * l + 0];
             const int plen = hi[8 * l + 4];
-            u.path.assign(hpath.begin() + (size_t)path_cap * l, hpath.begin() + (size_t)path_cap * l + plen);
+            if (plen < 0 || (size_t)plen > pstride) return set_err(LB_INTERNAL, "best path length out of range");
+            u.path.assign(hpath.begin() + pstride * l, hpath.begin() + pstride * l + plen);
             if (lat) {
                 rc = finalize_device(g, desc[l], T[w0 + l], D, cfg->acoustic_scale, cfg->lattice_beam, u.partial, fl,
                                      st, u, n - (w0 + l));
@@ -1083,7 +1108,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         }
         cudaFree(d_prof);
     }
-    return LB_OK;
+    return guard_round_tags(w, st);
 }
 
 }  // namespace
@@ -1248,6 +1273,7 @@ int lb_graph_destroy(lb_graph *g) {
     cudaSetDevice(g->device);
     if (g->bexec) cudaGraphExecDestroy(g->bexec);
     g->ws.release();
+    g->ws1.release();
     cudaFree(g->arcs);
     cudaFree(g->src);
     cudaFree(g->ol);
@@ -1374,11 +1400,20 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     std::vector<std::thread> th;
     std::vector<const double *> dptr(n);
     float h2d = 0.0f;
+    // joins the staging threads on every path out of this function (an unjoined
+    // std::thread would terminate the process)
+    struct Joiner {
+        std::vector<std::thread> &v;
+        ~Joiner() {
+            for (auto &t : v)
+                if (t.joinable()) t.join();
+        }
+    } joiner{th};
     if (progressive) {
-        for (unsigned w = 0; w < nth; w++) th.emplace_back(work, w);
         double *dev = nullptr;
-        CK(cudaHostGetDevicePointer((void **)&dev, g->h_stage, 0));
+        CK(cudaHostGetDevicePointer((void **)&dev, g->h_stage, 0));   // before any thread starts
         for (int i = 0; i < n; i++) dptr[i] = dev + off[i];
+        for (unsigned w = 0; w < nth; w++) th.emplace_back(work, w);
         rc = decode_impl(g, n, dptr.data(), T, D, cfg, g->stream, res.get(), 0.0f, g->d_ready);
         for (auto &t : th) t.join();   // the kernel finished, so every chunk was published
         res->t_h2d = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_stage).count();
@@ -1770,9 +1805,9 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     std::lock_guard<std::mutex> lock(g->mu);
     CK(cudaSetDevice(g->device));
     const int64_t ccap = std::min<int64_t>(g->A_emit, n * g->max_edeg) + 25 * CAND_CHUNK;
-    int rc = ensure_workspace(g, 1, 1, ccap, n + g->S, 0, 16, 1, false, false);
+    int rc = ensure_workspace(g, g->ws1, 1, 1, ccap, n + g->S, 0, 16, 1, false, false);
     if (rc) return rc;
-    Workspace &w = g->ws;
+    Workspace &w = g->ws1;
     cudaStream_t st = g->stream;
     double *d_row = nullptr;
     if (mode == 0) {
@@ -1813,6 +1848,7 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     CK(cudaMemcpy(out_costs, d.tok_cost + n, 8 * (size_t)m, cudaMemcpyDeviceToHost));
     for (int k = 0; k < m; k++) out_states[k] = (int32_t)os[k];
     *n_out = m;
+    if (int rg = guard_round_tags(w, st)) return rg;
     if (cutoff_out) *cutoff_out = od[0];
     return LB_OK;
 }

@@ -223,9 +223,11 @@ CONFIGS = {
                frames=300, utts=1, want_lattice=True),
     "C4": dict(graph=("hclg", dict(seed=0)), decode=dict(beam=13.0, lattice_beam=8.0, max_active=7000),
                frames=300, utts=4096, want_lattice=False),
+    # ~1000 backoff hubs with epsilon in-degree ~8.5k each (most states carry an
+    # epsilon "backoff" arc into a hub, as an LM graph does)
     "C5": dict(graph=("hclg", dict(seed=0, num_states=15_000_000, pool_size=60_000, pool_fwd=8,
-                                   cold_fwd_mean=1.9, eps_per_state=0.45, eps_depth=8,
-                                   num_hubs=1000, hub_share=0.3)),
+                                   cold_fwd_mean=1.6, eps_per_state=0.8, eps_depth=8,
+                                   num_hubs=1000, hub_share=0.8)),
                decode=dict(beam=16.0, lattice_beam=8.0, max_active=20_000), frames=300, utts=1,
                want_lattice=False),
 }

@@ -393,3 +393,58 @@ def test_compute_sanitizer_clean(tool):
     assert res.returncode == 0, out[-6000:]
     clean = "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards displayed (0 errors" in out
     assert "ok" in res.stdout and clean, out[-3000:]
+
+
+A4_GRAPH = "3 1 1 1 1.0\n3 2 1 2 1.0000000000009095\n1 2 0 0 0.0\n2 1 0 0 0.0\n1 0.0\n2 0.0\n"
+
+
+@pytest.mark.parametrize("mode", ["batched", "lane"])
+@pytest.mark.parametrize("want_lattice", [False, True])
+def test_backtrace_cycle_raises_on_device(oracle_mod, monkeypatch, mode, want_lattice):
+    """states 1 and 2 end up as each other's epsilon
+    predecessor (f32-equal costs, lower arc ids win the ties), so the reference's
+    _backtrace never terminates.  The device walk is step-bounded and reports
+    InternalInvariantError, as the oracle does."""
+    monkeypatch.setenv("LB_MODE", mode)
+    w = lb.load_wfst_text(A4_GRAPH)
+    m = lb.load_cost_matrix("1 1\n0.0\n")
+    ref = oracle_mod.decode(w, m, 10.0, want_lattice=False)
+    assert ref.status == 4 and "backtrace" in ref.message
+    with pytest.raises(lb.InternalInvariantError, match="backtrace"):
+        lb.decode_utterance(w, m, lb.DecodeConfig(beam=10.0), want_lattice=want_lattice)
+    # the graph stays usable afterwards (the error path reset its lane state)
+    ok = lb.load_wfst_text("0 1 1 1 0.5\n0 2 2 2 1.0\n1 0.0\n2 0.0\n")
+    r = lb.decode_utterance(ok, lb.load_cost_matrix("1 2\n0.3 0.1\n"), lb.DecodeConfig())
+    assert r.words == [1]
+
+
+@pytest.mark.parametrize("mode", ["batched", "lane"])
+def test_shorter_batch_after_longer_batch(oracle_mod, monkeypatch, mode):
+    """A workspace grown by a batch of long utterances is reused by a later batch of
+    shorter ones: every lane's best path (words, alignment) still matches the
+    oracle (the path buffer stride is the workspace's, not the call's)."""
+    monkeypatch.setenv("LB_MODE", mode)
+    w = synthetic.hclg_graph(6, num_states=100_000, pool_size=2000, num_pdfs=300)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=800)
+    for T, n in ((160, 12), (40, 12), (90, 5), (25, 12)):
+        mats = [synthetic.hclg_matrix(3000 + 100 * T + i, num_frames=T - (i % 3), num_pdfs=300)
+                for i in range(n)]
+        res = lb.decode_batch(w, mats, cfg, want_lattice=False)
+        for m, r in zip(mats, res):
+            ref = oracle_mod.decode(w, m, 12.0, max_active=800, want_lattice=False, collect_frames=False)
+            assert ref.ok
+            assert r.words == ref.words and r.alignment == ref.alignment, (T, n)
+            assert r.total_cost == ref.total_cost
+
+
+def test_epsilon_round_tags_reset(oracle_mod, monkeypatch):
+    """Round tags are reset (LB_FORCE_TAG_RESET forces it after every decode);
+    decodes before and after a reset equal the oracle."""
+    monkeypatch.setenv("LB_FORCE_TAG_RESET", "1")
+    w = synthetic.hclg_graph(3, num_states=50_000, pool_size=1500, num_pdfs=200)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600)
+    for k in range(3):
+        mats = [synthetic.hclg_matrix(4000 + 10 * k + i, num_frames=30, num_pdfs=200) for i in range(6)]
+        res = lb.decode_batch(w, mats, cfg, want_lattice=False)
+        tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
+        assert all(st == 0) and [r.total_cost for r in res] == tc.tolist()
