@@ -79,6 +79,20 @@ int lb_decode_batch_device(const lb_graph *g, int32_t n_utts, const double *cons
                            const int32_t *num_frames, int32_t num_labels, const lb_config *cfg,
                            void *stream, lb_result **out);
 
+/* decode_batch across devices: graphs[k] is a replica of the
+ * same graph on some device (lb_graph_create per device; the same device may
+ * hold several replicas).  Utterances are split longest-first (lb_shard_lpt),
+ * each replica decodes its shard on its own host thread, and the result holds
+ * every utterance in input order.  No collective: utterances share nothing
+ * (decoder.py:644-672, the reference's pool over utterances). */
+int lb_decode_batch_multi(const lb_graph *const *graphs, int32_t n_graphs, int32_t n_utts,
+                          const double *const *costs, const int32_t *num_frames, int32_t num_labels,
+                          const lb_config *cfg, lb_result **out);
+/* The LPT assignment lb_decode_batch_multi uses: utterances by descending length
+ * (ties: input order), each to the shard with the fewest frames so far (ties:
+ * lowest shard).  shard_of[i] in [0, n_shards).  Host-only. */
+int lb_shard_lpt(int32_t n_utts, const int32_t *num_frames, int32_t n_shards, int32_t *shard_of);
+
 /* Per-utterance readback.  DecodeResult (decoder.py:92-103). */
 int lb_result_count(const lb_result *r, int32_t *n_utts);
 int lb_result_status(const lb_result *r, int32_t utt, int32_t *status, char *message,

@@ -1456,6 +1456,86 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     return LB_OK;
 }
 
+// Longest-processing-time-first split of utterances over shards (devices):
+// utterances in descending length (ties: input order) each go to the shard with
+// the fewest frames so far (ties: lowest shard).  Deterministic.
+int lb_shard_lpt(int32_t n, const int32_t *T, int32_t n_shards, int32_t *shard_of) {
+    if (n < 0 || n_shards < 1 || (n > 0 && (!T || !shard_of))) return set_err(LB_USAGE, "bad shard arguments");
+    std::vector<int32_t> ord(n);
+    for (int i = 0; i < n; i++) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return T[a] > T[b]; });
+    std::vector<long long> load(n_shards, 0);
+    for (int32_t i : ord) {
+        int best = 0;
+        for (int s = 1; s < n_shards; s++)
+            if (load[s] < load[best]) best = s;
+        shard_of[i] = best;
+        load[best] += std::max(T[i], 0);
+    }
+    return LB_OK;
+}
+
+// decode_batch over several graph replicas (one per device):
+// LPT shards, one host thread per replica (each an independent lb_decode_batch on
+// its device), results merged back into input order.  No collective: utterances
+// share nothing (decoder.py:644-672).
+int lb_decode_batch_multi(const lb_graph *const *graphs, int32_t n_graphs, int32_t n, const double *const *costs,
+                          const int32_t *T, int32_t D, const lb_config *cfg, lb_result **out) {
+    if (!graphs || n_graphs < 1 || !out) return set_err(LB_USAGE, "graphs/out is NULL");
+    *out = nullptr;
+    for (int k = 0; k < n_graphs; k++)
+        if (!graphs[k]) return set_err(LB_USAGE, "graph replica is NULL");
+    if (n < 0) return set_err(LB_USAGE, "n_utts must be >= 0");
+    if (n_graphs == 1) return lb_decode_batch(graphs[0], n, costs, T, D, cfg, out);
+    std::vector<int32_t> shard(n);
+    if (int rc = lb_shard_lpt(n, T, n_graphs, shard.data())) return rc;
+    std::vector<std::vector<int32_t>> idx(n_graphs);
+    for (int i = 0; i < n; i++) idx[shard[i]].push_back(i);
+    std::vector<lb_result *> part(n_graphs, nullptr);
+    std::vector<int> rcs(n_graphs, LB_OK);
+    std::vector<std::string> msgs(n_graphs);
+    auto run = [&](int k) {
+        const auto &ix = idx[k];
+        std::vector<const double *> c(ix.size());
+        std::vector<int32_t> t(ix.size());
+        for (size_t j = 0; j < ix.size(); j++) {
+            c[j] = costs[ix[j]];
+            t[j] = T[ix[j]];
+        }
+        rcs[k] = lb_decode_batch(graphs[k], (int32_t)ix.size(), c.data(), t.data(), D, cfg, &part[k]);
+        if (rcs[k]) msgs[k] = g_err;   // the message is thread-local
+    };
+    {
+        std::vector<std::thread> th;
+        for (int k = 1; k < n_graphs; k++) th.emplace_back(run, k);
+        run(0);
+        for (auto &x : th) x.join();
+    }
+    std::unique_ptr<lb_result> res(new lb_result());
+    res->utts.resize(n);
+    int first = LB_OK;
+    std::string first_msg;
+    for (int k = 0; k < n_graphs; k++) {
+        if (rcs[k] && first == LB_OK) {
+            first = rcs[k];
+            first_msg = msgs[k];
+        }
+        if (!part[k]) continue;
+        lb_result &p = *part[k];
+        for (size_t j = 0; j < idx[k].size(); j++) res->utts[idx[k][j]] = std::move(p.utts[j]);
+        // the replicas run concurrently: the call's device time is the slowest one's
+        res->t_decode = std::max(res->t_decode, p.t_decode);
+        res->t_prune = std::max(res->t_prune, p.t_prune);
+        res->t_h2d = std::max(res->t_h2d, p.t_h2d);
+        res->t_d2h = std::max(res->t_d2h, p.t_d2h);
+        res->launches += p.launches;
+        delete part[k];
+    }
+    if (first != LB_OK) return set_err(first, first_msg);
+    *out = res.release();
+    return LB_OK;
+}
+
 int lb_decode_batch_device(const lb_graph *gc, int32_t n, const double *const *dev_costs, const int32_t *T,
                            int32_t D, const lb_config *cfg, void *stream, lb_result **out) {
     lb_graph *g = const_cast<lb_graph *>(gc);

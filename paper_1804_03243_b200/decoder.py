@@ -45,7 +45,9 @@ class DecodeConfig:
     DESIGN.md §3), `token_arena` (tokens kept per utterance over all frames,
     0 = auto), `lanes` (utterances in flight per launch, 0 = auto),
     `threads_per_lane` (CTA size 512/640/768, 0 = 640), `ctas_per_lane` (thread-block
-    cluster size of a lane, 0 = auto), `device` (CUDA ordinal),
+    cluster size of a lane, 0 = auto), `device` (CUDA ordinal), `devices`
+    (several ordinals: `decode_batch` shards the utterances over one graph replica
+    per entry, longest first, and returns them in input order),
     `keep_work_lattice` (also return `DecodeResult.work_lattice`, every live
     arc with its extra cost; the final lattice is always built on the device).
     """
@@ -67,6 +69,7 @@ class DecodeConfig:
     ctas_per_lane: int = 0
     device: int = 0
     keep_work_lattice: bool = False
+    devices: tuple = ()
 
     def validate(self) -> None:
         if not (math.isfinite(self.beam) and self.beam > 0):
@@ -86,6 +89,9 @@ class DecodeConfig:
                      "device"):
             if int(getattr(self, name)) < 0:
                 raise UsageError(f"{name} must be >= 0")
+        devs = tuple(self.devices or ())
+        if any(int(d) < 0 for d in devs):
+            raise UsageError("devices must be CUDA ordinals >= 0")
         if int(self.threads_per_lane) not in (0, 512, 640, 768):
             raise UsageError("threads_per_lane must be 512, 640 or 768")
         if not 0 <= int(self.ctas_per_lane) <= 8:
@@ -158,16 +164,41 @@ _graph_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 _cache_lock = threading.Lock()
 
 
-def device_graph(wfst, device: int = 0) -> DeviceGraph:
-    """The cached replica of `wfst` on `device` (uploaded once per graph object)."""
+def device_graph(wfst, device: int = 0, replica: int = 0) -> DeviceGraph:
+    """The cached replica of `wfst` on `device` (uploaded once per graph object);
+    `replica` > 0 asks for an additional, independent replica on the same device
+    (own workspace and stream, so decodes on it run concurrently)."""
     if isinstance(wfst, DeviceGraph):
         return wfst
     with _cache_lock:
         per = _graph_cache.setdefault(wfst, {})
-        g = per.get(device)
+        key = (int(device), int(replica))
+        g = per.get(key)
         if g is None:
-            g = per[device] = DeviceGraph(wfst, device)
+            g = per[key] = DeviceGraph(wfst, device)
         return g
+
+
+def device_replicas(wfst, devices) -> list:
+    """One replica per entry of `devices` (a device listed twice gets two)."""
+    seen: dict = {}
+    out = []
+    for d in devices:
+        k = seen.get(int(d), 0)
+        seen[int(d)] = k + 1
+        out.append(device_graph(wfst, int(d), k))
+    return out
+
+
+def shard_lpt(lengths, n_shards: int) -> np.ndarray:
+    """The longest-first utterance split the multi-device decode uses
+    (lb_shard_lpt): shard index per utterance."""
+    T = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = np.zeros(len(T), dtype=np.int32)
+    rc = _lib.host_lib().lb_shard_lpt(len(T), ptr(T, P32), int(n_shards), ptr(out, P32))
+    if rc != 0:
+        raise UsageError("bad shard arguments")
+    return out
 
 
 def _raise_status(rc: int, msg: str, bound: str = "") -> None:
@@ -217,14 +248,22 @@ def decode_batch(wfst, matrices, config: DecodeConfig | None = None, want_lattic
         raise UsageError(f"graph uses input label {wfst.max_ilabel} but the cost matrix "
                          f"has only {D} columns")
     t0 = time.perf_counter()
-    g = device_graph(wfst, cfg.device)
     L = _lib.lib()
     n = len(mats)
     cptrs = (PD * n)(*[ptr(m, PD) for m in mats])
     T = np.asarray([m.shape[0] for m in mats], dtype=np.int32)
     c = cfg.to_c(want_lattice, collect_frame_packs)
     res = PV()
-    rc = L.lb_decode_batch(g.handle, n, cptrs, ptr(T, P32), D, C.byref(c), C.byref(res))
+    devs = tuple(cfg.devices or ())
+    if len(devs) > 1:
+        # one replica per device, LPT shards on one host thread each (ctypes
+        # releases the GIL; the threads live in the native library)
+        reps = device_replicas(wfst, devs)
+        hs = (PV * len(reps))(*[r.handle for r in reps])
+        rc = L.lb_decode_batch_multi(hs, len(reps), n, cptrs, ptr(T, P32), D, C.byref(c), C.byref(res))
+    else:
+        g = device_graph(wfst, devs[0] if devs else cfg.device)
+        rc = L.lb_decode_batch(g.handle, n, cptrs, ptr(T, P32), D, C.byref(c), C.byref(res))
     _raise_status(rc, _lib.last_error())
     try:
         out = collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs,
