@@ -1,19 +1,29 @@
 """Benchmark: decoded frames/s (and arcs/s) of the B200 decoder on config C4.
 
-Workload (BASELINE.json configs[3], "sequence-parallel batch"): the C2/C3
-HCLG-shaped graph (5M states, ~14.7M arcs, 3000 pdfs, acyclic epsilons),
-beam 13, max-active 7000, 1-best, T=300-frame utterances of i.i.d. U(0,5) f64
-acoustic costs.  One step = one batch of `--utts` utterances decoded to the
-end on every GPU (one decode lane per utterance; weak scaling over ranks).
+Workload (BASELINE.json configs[3], "sequence-parallel batch: 64 concurrent
+decode lanes per GPU, 4096 utterances sharded over 1/2/4/8 B200"): the C2/C3
+HCLG-shaped graph (5M states, ~14.7M arcs, 3000 pdfs, acyclic epsilons), beam
+13, max-active 7000, 1-best, T=300-frame utterances of i.i.d. U(0,5) f64
+acoustic costs.  One step = the WHOLE 4096-utterance job: each rank takes its
+longest-first shard of the utterance list (the same LPT split the multi-device
+decode_batch uses) and decodes it in ONE call on 64 refilling decode lanes.
+Total work is fixed as N grows, so `scaling` is "strong".
 
   value  frames/s with the cost matrices already resident in HBM (C-ABI
          lb_decode_batch_device, CUDA events on the launching stream, L2
          flushed between steps), max over ranks, whole box.
   e2e    the same metric through the public API `decode_batch` on host numpy
-         matrices: H2D of the costs and D2H of the results inside the timed region.
+         matrices: the streamed pinned staging of the costs (H2D) and the D2H of
+         the results are inside the timed region.
+
+The synthetic utterances cycle through a pool of distinct seeded matrices (one
+decode per utterance, nothing is cached between decodes).  `--ragged` draws
+T uniformly from [100, 500] instead of 300 (the refilling scheduler's case).
 
 `--impl reference` times the reference algorithm's CPU path instead (the
-oracle/ C port of latbeam's decoder, all host threads), on a bounded sample.
+oracle/ C port of latbeam's decoder with the max-active extension, all host
+threads), on the first utterances of the same list (same graph, same 300-frame
+utterances).
 
     python bench.py [--gpus N --steps K --warmup W]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -38,6 +48,7 @@ sys.path.insert(0, ROOT)
 METRIC = "decoded frames/sec & arcs/sec (whole box) at 1/2/4/8 B200 vs CPU reference"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "decode_kernel_traffic.json")
+D_PDFS = 3000
 
 
 def bytes_of(c):
@@ -48,24 +59,32 @@ def bytes_of(c):
             + 16 * c[7])
 
 
+def exp_bytes_of(c):
+    """Arc-expansion bytes only (SURVEY.md §8(d) B_exp = 28 N + 16 N_scan + 8 N_cand)."""
+    return 28 * c[0] + 16 * c[1] + 8 * c[2]
+
+
 def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--utts", type=int, default=int(os.environ.get("LB_BENCH_UTTS", 64)),
-                   help="utterances per step per GPU (= decode lanes)")
+    p.add_argument("--utts", type=int, default=int(os.environ.get("LB_BENCH_UTTS", 4096)),
+                   help="utterances of the whole job (all ranks)")
+    p.add_argument("--pool", type=int, default=256, help="distinct utterance matrices the job cycles through")
     p.add_argument("--frames", type=int, default=300)
-    p.add_argument("--lanes", type=int, default=0)
+    p.add_argument("--ragged", action="store_true", help="T ~ U[100, 500] per utterance")
+    p.add_argument("--lanes", type=int, default=64, help="concurrent decode lanes per GPU")
     p.add_argument("--threads", type=int, default=0, help="threads per CTA of a lane")
     p.add_argument("--ctas", type=int, default=0, help="CTAs (thread-block cluster size) per lane")
     p.add_argument("--states", type=int, default=5_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-utts", type=int, default=0)
-    p.add_argument("--cpu-frames", type=int, default=100)
-    p.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C3 side measurements")
+    p.add_argument("--cpu-frames", type=int, default=0, help="frames per CPU utterance (0 = the job's)")
+    p.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C3/ragged side measurements")
+    p.add_argument("--no-phases", action="store_true", help="skip the phase-split (arc-expansion) run")
     p.add_argument("--all-configs", action="store_true", help="also measure C5 (builds the 50M-arc graph)")
     return p.parse_args(argv)
 
@@ -113,11 +132,18 @@ class Dist:
             self.pg.destroy_process_group()
 
 
-def shard_seeds(rank: int, step: int, utts: int, pool: int) -> list[int]:
-    """Utterance seeds of one rank's step: disjoint across ranks (rank-major),
-    cycling through a pool of `pool` distinct utterances per rank."""
-    base = 100 + rank * 1_000_000
-    return [base + (step * utts + i) % pool for i in range(utts)]
+def utterance_lengths(n: int, frames: int, ragged: bool, seed: int = 11) -> np.ndarray:
+    if not ragged:
+        return np.full(n, frames, dtype=np.int32)
+    return np.random.default_rng(seed).integers(100, 501, size=n).astype(np.int32)
+
+
+def rank_utterances(rank: int, world: int, n: int, lengths=None) -> list:
+    """Utterances of the job this rank decodes: its shard of the longest-first
+    split (decoder.shard_lpt == the C-ABI lb_shard_lpt of lb_decode_batch_multi)."""
+    from paper_1804_03243_b200.decoder import split_batch
+    T = np.full(n, 300, dtype=np.int32) if lengths is None else np.asarray(lengths, dtype=np.int32)
+    return split_batch(T, world)[rank]
 
 
 class ClockSampler:
@@ -174,21 +200,37 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_sample(graph, og, beam, max_active, n_utts, frames, seed_base=100):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_pool(n_pool: int, max_frames: int):
+    """Distinct seeded matrices (hclg_matrix(100 + i)); utterance u uses pool[u % n_pool][:T_u]."""
+    from paper_1804_03243_b200 import synthetic
+    return [np.ascontiguousarray(synthetic.hclg_matrix(100 + i, num_frames=max_frames, num_pdfs=D_PDFS).costs)
+            for i in range(n_pool)]
+
+
+def cpu_sample(graph, og, beam, max_active, mats, threads):
     """Time the oracle C port (the reference algorithm) on host threads."""
     from oracle import oracle as O
-    from paper_1804_03243_b200 import synthetic
-    threads = cpu_threads()
-    mats = [synthetic.hclg_matrix(seed_base + i, num_frames=frames) for i in range(n_utts)]
     t0 = time.perf_counter()
     tc, st, cnt = O.decode_batch_mt(graph, mats, beam, max_active=max_active, want_lattice=False,
                                     nthreads=threads, graph=og)
     dt = time.perf_counter() - t0
-    return dt, n_utts * frames, int(cnt[:, 1].sum() + cnt[:, 4].sum()), threads, st
+    return dt, int(sum(m.shape[0] for m in mats)), int(cnt[:, 1].sum() + cnt[:, 4].sum()), st
 
 
 def run_reference(args, dist: Dist):
-    """`--impl reference`: the reference decoder's algorithm on the host CPU."""
+    """`--impl reference`: the reference decoder's algorithm on the host CPU,
+    one utterance per host thread (the reference's decode_batch pool), each step
+    the next `threads` utterances of the job's list at their full length."""
     if dist.rank != 0:
         dist.close()
         return
@@ -198,21 +240,29 @@ def run_reference(args, dist: Dist):
     og = O.OracleGraph(graph)
     threads = cpu_threads()
     n = args.cpu_utts or threads
-    for _ in range(args.warmup):
-        cpu_sample(graph, og, 13.0, 7000, min(n, threads), 10)
+    lengths = utterance_lengths(args.utts, args.frames, args.ragged)
+    frames = args.cpu_frames or None
+    pool = host_pool(min(args.pool, n * (args.steps + 1)), int(lengths.max()))
+
+    def mats_of(k):
+        ids = [(k * n + i) % args.utts for i in range(n)]
+        return [pool[u % len(pool)][:(frames or lengths[u])] for u in ids]
+
+    cpu_sample(graph, og, 13.0, 7000, [m[:20] for m in mats_of(0)], threads)   # warm-up (page-in)
     total_t, total_f, total_a = 0.0, 0, 0
     for k in range(args.steps):
-        dt, fr, arcs, _, st = cpu_sample(graph, og, 13.0, 7000, n, args.cpu_frames, seed_base=100 + k * n)
+        dt, fr, arcs, st = cpu_sample(graph, og, 13.0, 7000, mats_of(k), threads)
         total_t += dt
         total_f += fr
         total_a += arcs
     v = total_f / total_t
-    sample = f"{n} utterances x {args.cpu_frames} frames per step on {threads} threads (oracle C port)"
+    sample = (f"{n} utterances x {frames or 'full-length'} frames of the job's list per step, one per host thread "
+              f"({threads} threads, {cpu_model()}), oracle C port of the reference decoder")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "arcs_per_sec": total_a / total_t,
-           "config": config_dict(args, note="CPU sample of the same workload"),
+           "config": config_dict(args, note="CPU sample of the same workload (same graph and utterances)"),
            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
                             "sample": sample},
            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -255,17 +305,47 @@ def measure_configs(graph_c2, all_configs: bool) -> dict:
            "C2": run("C2", graph_c2, 1, False),
            "C3": run("C3", graph_c2, 1, True)}
     if all_configs:
-        res["C5"] = run("C5", synthetic.config_graph("C5"), 1, False)
+        g5 = synthetic.config_graph("C5")
+        res["C5"] = run("C5", g5, 1, False)
+        res["C5_batch"] = c5_batch_roofline(g5)
     res["note"] = "public API decode_batch, host costs, wall clock incl. H2D/D2H and host result assembly"
     return res
 
 
+def c5_batch_roofline(g5, n_utts: int = 128, lanes: int = 64) -> dict:
+    """C5 (50M arcs, ~1000 epsilon hubs of in-degree ~8.5k, beam 16, max-active
+    20k) as a multi-utterance job: HBM-resident costs, 64 refilling lanes; the
+    decode kernel's algorithmic bytes over its event time."""
+    import torch
+
+    import paper_1804_03243_b200 as lb
+    from paper_1804_03243_b200 import synthetic
+    from paper_1804_03243_b200.resident import decode_batch_resident
+    d = synthetic.CONFIGS["C5"]["decode"]
+    pool = [torch.from_numpy(np.ascontiguousarray(synthetic.config_matrix("C5", u).costs)).cuda()
+            for u in range(16)]
+    tens = [pool[u % len(pool)] for u in range(n_utts)]
+    cfg = lb.DecodeConfig(beam=d["beam"], max_active=d["max_active"], lanes=lanes)
+    decode_batch_resident(g5, tens, cfg)
+    torch.cuda.synchronize()
+    outs, tm = decode_batch_resident(g5, tens, cfg)
+    alg = sum(bytes_of(o["counters"]) for o in outs)
+    peak = json.load(open(PEAKS)).get("hbm_gbs", 6650.0) if os.path.exists(PEAKS) else 6650.0
+    frames = sum(int(t.shape[0]) for t in tens)
+    ach = alg / (tm["decode_ms"] / 1e3) / 1e9
+    return {"utterances": n_utts, "lanes": lanes, "frames": frames, "frames_per_s": frames / (tm["decode_ms"] / 1e3),
+            "kernel_ms": tm["decode_ms"], "alg_bytes": alg, "achieved_gbs": ach, "frac": ach / peak,
+            "status_ok": all(o["status"] == 0 for o in outs)}
+
+
 def config_dict(args, note=""):
-    d = {"workload": "C4: sequence-parallel batch on the C2 HCLG graph (1-best, beam 13, max-active 7000)",
+    d = {"workload": f"C4: one {args.utts}-utterance job on the C2 HCLG graph (1-best, beam 13, max-active 7000), "
+                     f"{args.lanes} refilling decode lanes per GPU, utterances sharded longest-first over ranks",
          "graph": f"hclg_graph(seed=0, states={args.states}), 3000 pdfs, acyclic epsilon depth<=4",
-         "utts_per_step_per_gpu": args.utts, "frames_per_utt": args.frames, "beam": 13.0,
-         "max_active": 7000, "lanes": args.lanes or "auto", "threads_per_cta": args.threads or 640,
-         "ctas_per_lane": args.ctas or 2,
+         "utterances": args.utts,
+         "frames_per_utt": "U[100,500]" if args.ragged else args.frames,
+         "distinct_matrices": args.pool, "beam": 13.0, "max_active": 7000, "lanes_per_gpu": args.lanes,
+         "threads_per_cta": args.threads or 640, "ctas_per_lane": args.ctas or 2,
          "l2": "flushed between steps (256 MiB write); graph 0.36 GB > L2"}
     if note:
         d["note"] = note
@@ -290,11 +370,13 @@ def main(argv=None):
     cfg = lb.DecodeConfig(beam=13.0, max_active=7000, lanes=args.lanes, threads_per_lane=args.threads,
                           ctas_per_lane=args.ctas, device=dev)
     lb.device_graph(graph, dev)
-    U, T = args.utts, args.frames
-    pool = 2 * U
-    seeds = sorted({s for k in range(pool) for s in shard_seeds(dist.rank, k, U, pool)})
-    host = {s: np.ascontiguousarray(synthetic.hclg_matrix(s, num_frames=T).costs) for s in seeds}
-    resident = {s: torch.from_numpy(a).to(f"cuda:{dev}") for s, a in host.items()}
+    lengths = utterance_lengths(args.utts, args.frames, args.ragged)
+    mine = rank_utterances(dist.rank, dist.world, args.utts, lengths)
+    pool = host_pool(min(args.pool, args.utts), int(lengths.max()))
+    host = [pool[u % len(pool)][:lengths[u]] for u in mine]
+    dpool = [torch.from_numpy(m).to(f"cuda:{dev}") for m in pool]
+    resident = [dpool[u % len(pool)][:lengths[u]] for u in mine]
+    frames_mine = int(sum(int(lengths[u]) for u in mine))
     # the other configs first, in a fresh process state (each has its own warm-up)
     configs = None
     if dist.rank == 0 and dist.world == 1 and not args.no_configs:
@@ -303,29 +385,28 @@ def main(argv=None):
     stream = torch.cuda.Stream(device=dev)     # the decode kernels and the timing events share it
     torch.cuda.set_stream(stream)
 
-    def step_resident(k):
-        outs, tm = decode_batch_resident(graph, [resident[s] for s in shard_seeds(dist.rank, k, U, pool)],
-                                         cfg, stream=stream)
+    def step_resident(tens, c=cfg):
+        outs, tm = decode_batch_resident(graph, tens, c, stream=stream)
         bad = [o for o in outs if o["status"] != 0]
         if bad:
             raise RuntimeError(f"decode failed in bench step: {bad[0]}")
         return outs, tm
 
     for k in range(args.warmup):
-        step_resident(k)
+        step_resident(resident)
     torch.cuda.synchronize()
     clocks = ClockSampler(dev)
     clocks.start()
     dist.barrier()
     torch.cuda.synchronize()
-    total_ms, kern_ms, launches, alg_bytes, arcs, host_ms = 0.0, 0.0, 0, 0, 0, 0.0
+    total_ms, kern_ms, launches, alg_bytes, exp_bytes, arcs, host_ms = 0.0, 0.0, 0, 0, 0, 0, 0.0
     for k in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         h0 = time.perf_counter()
-        outs, tm = step_resident(args.warmup + k)
+        outs, tm = step_resident(resident)
         host_ms += (time.perf_counter() - h0) * 1e3
         e1.record(stream)
         torch.cuda.synchronize()
@@ -334,21 +415,20 @@ def main(argv=None):
         launches += tm["launches"]
         for o in outs:
             alg_bytes += bytes_of(o["counters"])
+            exp_bytes += exp_bytes_of(o["counters"])
             arcs += int(o["counters"][1] + o["counters"][4])
     torch.cuda.synchronize()
     dist.barrier()
     ck = clocks.stop()
     t_max = dist.max(total_ms)
-    frames_all = dist.sum(U * T * args.steps)
+    frames_all = dist.sum(frames_mine * args.steps)
     arcs_all = dist.sum(arcs)
     value = frames_all / (t_max / 1e3)
 
-    # ---- e2e through the public API (host matrices, H2D + D2H inside) ----
+    # ---- e2e through the public API (host matrices, streamed H2D + D2H inside) ----
     e2e = None
     if not args.no_e2e:
-        for k in range(1):
-            lb.decode_batch(graph, [host[s] for s in shard_seeds(dist.rank, k, U, pool)], cfg,
-                            want_lattice=False)
+        lb.decode_batch(graph, host, cfg, want_lattice=False)
         torch.cuda.synchronize()
         dist.barrier()
         t_e2e = 0.0
@@ -356,17 +436,16 @@ def main(argv=None):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res = lb.decode_batch(graph, [host[s] for s in shard_seeds(dist.rank, args.warmup + k, U, pool)],
-                                  cfg, want_lattice=False)
+            res = lb.decode_batch(graph, host, cfg, want_lattice=False)
             torch.cuda.synchronize()
             t_e2e += time.perf_counter() - t0
             assert all(r.total_cost == r.total_cost for r in res)
         t_e2e = dist.max(t_e2e)
-        path_cap = 4 * T + 256
+        path_cap = 4 * int(lengths.max()) + 256
         e2e = {"value": frames_all / t_e2e, "unit": "frames/s",
-               "h2d_bytes_per_step": U * T * 3000 * 8,
-               "d2h_bytes_per_step": U * (8 * 4 + 4 * 8 + 8 * 8 + 4 * path_cap),
-               "path": "paper_1804_03243_b200.decode_batch (host numpy f64 costs)"}
+               "h2d_bytes_per_step": int(dist.sum(frames_mine * D_PDFS * 8)),
+               "d2h_bytes_per_step": int(dist.sum(len(mine) * (8 * 4 + 4 * 8 + 8 * 8 + 4 * path_cap))),
+               "path": "paper_1804_03243_b200.decode_batch (host numpy f64 costs, streamed pinned ring)"}
 
     # ---- roofline of the dominant kernel (decode_kernel) ----
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
@@ -380,26 +459,92 @@ def main(argv=None):
                 "kernel": "decode_kernel", "alg_bytes_per_launch": alg_bytes / max(args.steps, 1),
                 "kernel_ms_per_launch": kern_ms / max(args.steps, 1),
                 "step_host_ms": host_ms / max(args.steps, 1),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback"}
+
+    # ---- arc-expansion roofline: B_exp over the emit phase's share of the lanes' time ----
+    if dist.rank == 0 and not args.no_phases:
+        roofline["arc_expansion"] = phase_split(graph, resident, cfg, peak, step_resident)
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         from oracle import oracle as O
         og = O.OracleGraph(graph)
-        n = args.cpu_utts or cpu_threads()
-        dt, fr, _, threads, _ = cpu_sample(graph, og, 13.0, 7000, n, args.cpu_frames)
+        threads = cpu_threads()
+        n = args.cpu_utts or threads
+        frames = args.cpu_frames or None
+        mats = [pool[u % len(pool)][:(frames or lengths[u])] for u in range(n)]
+        dt, fr, _, _ = cpu_sample(graph, og, 13.0, 7000, mats, threads)
         cpu = {"value": fr / dt, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"{n} utterances x {args.cpu_frames} frames, oracle C port on {threads} threads"}
+               "sample": f"{n} utterances x {frames or 'full-length'} frames of the job's list, "
+                         f"oracle C port on {threads} threads ({cpu_model()})"}
+
+    ragged = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_configs and not args.ragged:
+        ragged = ragged_variant(args, dpool, step_resident, flush)
 
     if dist.rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": dist.world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic", "arcs_per_sec": arcs_all / (t_max / 1e3),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": f"synthetic: seeded U(0,5) f64 costs, {args.utts} utterances cycling through "
+                       f"{min(args.pool, args.utts)} distinct matrices",
+               "arcs_per_sec": arcs_all / (t_max / 1e3),
                "config": config_dict(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": launches, "clocks": ck, "configs_measured": configs}
+               "gpu_launches": launches, "clocks": ck, "ragged_variant": ragged, "configs_measured": configs}
         print(json.dumps(out), flush=True)
     dist.close()
+
+
+def phase_split(graph, resident, cfg, peak, step_resident, n_sub: int = 512) -> dict:
+    """One unprofiled-clock phase-split run (LB_PHASE_PROFILE=1: the lane leader
+    reads %globaltimer at each phase boundary) on the first n_sub utterances:
+    the emit phase's lane-time share, and B_exp over the emit time per lane
+    (lanes run concurrently, so the aggregate expansion bandwidth is
+    sum(B_exp) / (sum of lane emit time / lanes))."""
+    os.environ["LB_PHASE_PROFILE"] = "1"
+    try:
+        outs, tm = step_resident(resident[:n_sub])
+    finally:
+        del os.environ["LB_PHASE_PROFILE"]
+    ph = tm["phases_ms"]
+    lanes = min(int(cfg.lanes or 64), len(outs))
+    bexp = sum(exp_bytes_of(o["counters"]) for o in outs)
+    lane_ms = sum(ph.values())
+    emit_ms_per_lane = ph["emit"] / lanes
+    ach = bexp / (emit_ms_per_lane / 1e3) / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "b_exp": bexp,
+            "emit_ms_per_lane": emit_ms_per_lane, "utterances": len(outs), "lanes": lanes,
+            "phase_share": {k: v / lane_ms for k, v in ph.items() if lane_ms > 0},
+            "kernel_ms_profiled": tm["decode_ms"],
+            "definition": "B_exp = 28 N + 16 N_scan + 8 N_cand summed over the utterances; emit time = "
+                          "sum over lanes of their emit-phase time / lanes (LB_PHASE_PROFILE run)"}
+
+
+def ragged_variant(args, dpool, step_resident, flush, steps: int = 2) -> dict:
+    """The same job with T ~ U[100, 500] (the refilling scheduler's case): frames/s
+    with HBM-resident costs, to compare with the equal-length value."""
+    import torch
+    lengths = utterance_lengths(args.utts, args.frames, True)
+    if int(lengths.max()) > int(dpool[0].shape[0]):
+        from paper_1804_03243_b200 import synthetic
+        dpool = [torch.from_numpy(np.ascontiguousarray(
+            synthetic.hclg_matrix(100 + i, num_frames=int(lengths.max()), num_pdfs=D_PDFS).costs)).cuda()
+            for i in range(len(dpool))]
+    tens = [dpool[u % len(dpool)][:lengths[u]] for u in range(args.utts)]
+    step_resident(tens)
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step_resident(tens)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    frames = int(lengths.sum()) * steps
+    return {"frames_per_s": frames / (ms / 1e3), "utterances": args.utts, "frames_per_step": int(lengths.sum()),
+            "lengths": "U[100,500]", "steps": steps}
 
 
 if __name__ == "__main__":

@@ -134,17 +134,28 @@ struct Workspace {
     int *tok_arc = nullptr, *tok_pred = nullptr, *lat_arc = nullptr, *lat_from = nullptr, *lat_to = nullptr;
     unsigned long long *tok_pack = nullptr, *ne_enc = nullptr;
     long long *tok_base = nullptr, *lat_base = nullptr, *out_c = nullptr;
-    int *path = nullptr, *out_i = nullptr;
-    double *out_d = nullptr;
     LaneWs *d_lanes = nullptr;
     UttDesc *d_desc = nullptr;
     LaneCtl *d_ctl = nullptr;   // batched mode: per-lane control blocks
     std::vector<void *> owned;
+    // per-job (utterance) outputs of a call and the job queue (ensure_jobs)
+    int jobs_cap = 0, jobs_pstride = 0;
+    int *j_path = nullptr, *j_out_i = nullptr, *queue = nullptr;
+    double *j_out_d = nullptr;
+    long long *j_out_c = nullptr;
+    UttJob *d_jobs = nullptr;
+    std::vector<void *> jowned;
 
+    void release_jobs() {
+        for (void *p : jowned) cudaFree(p);
+        jowned.clear();
+        jobs_cap = jobs_pstride = 0;
+    }
     void release() {
         for (void *p : owned) cudaFree(p);
         owned.clear();
         lanes = 0;
+        release_jobs();
     }
 };
 
@@ -192,6 +203,10 @@ struct lb_graph {
     size_t fl_expect = 0;                  // growth hint: bytes the rest of this decode will likely take
     int *h_ready = nullptr;   // progressive staging counter (mapped pinned)
     int *d_ready = nullptr;
+    double *ring = nullptr;   // streamed staging ring of refilling decodes (mapped pinned)
+    size_t ring_cap = 0;
+    int *ring_ctl = nullptr;  // [0] ready count, [32..] per-slot done marks (mapped pinned)
+    int ring_ctl_cap = 0;
     GraphDev dev() const {
         GraphDev g;
         g.arcs = arcs;
@@ -263,10 +278,6 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     }
     CK(A(&w.tok_base, (size_t)(tmax + 2) * nl));
     CK(A(&w.lat_base, (size_t)(tmax + 2) * nl));
-    CK(A(&w.path, (size_t)path_cap * nl));
-    CK(A(&w.out_i, 8 * nl));
-    CK(A(&w.out_d, 4 * nl));
-    CK(A(&w.out_c, 8 * nl));
     CK(A(&w.d_lanes, nl));
     CK(A(&w.d_desc, nl));
     CK(A(&w.d_ctl, nl));
@@ -361,11 +372,29 @@ UttDesc slot_desc(const Workspace &w, int l, const double *costs, int T, int64_t
         d.lat_extra = w.lat_extra + l * lc;
         d.tmp = w.tmp + l * lc;
     }
-    d.path = w.path + (size_t)l * w.path_cap;
-    d.out_i = w.out_i + 8 * l;
-    d.out_d = w.out_d + 4 * l;
-    d.out_c = w.out_c + 8 * l;
-    return d;
+    return d;   // path / out_* are the job's (ensure_jobs)
+}
+
+// Per-job output slots for n utterances with best paths of pstride arcs.
+int ensure_jobs(Workspace &w, int n, int pstride) {
+    n = std::max(n, 1);
+    if (w.jobs_cap >= n && w.jobs_pstride == pstride) return LB_OK;
+    w.release_jobs();
+    const int cap = std::max(n, w.jobs_cap);
+    auto A = [&](auto **p, size_t cnt) -> cudaError_t {
+        cudaError_t e = dalloc(p, cnt);
+        if (e == cudaSuccess) w.jowned.push_back((void *)*p);
+        return e;
+    };
+    CK(A(&w.j_path, (size_t)cap * pstride));
+    CK(A(&w.j_out_i, 8 * (size_t)cap));
+    CK(A(&w.j_out_d, 4 * (size_t)cap));
+    CK(A(&w.j_out_c, 8 * (size_t)cap));
+    CK(A(&w.d_jobs, (size_t)cap));
+    CK(A(&w.queue, 1));
+    w.jobs_cap = cap;
+    w.jobs_pstride = pstride;
+    return LB_OK;
 }
 
 void fill_message(UttHost &u, int code, int frame, double aux, const lb_config &cfg) {
@@ -784,7 +813,7 @@ int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
     const long long key = ((long long)C << 40) | ((long long)threads << 24) | (long long)dsm;
     auto it = g->cluster_fit.find(key);
     if (it != g->cluster_fit.end()) return it->second;
-    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, int);
+    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, const UttJob *, int, int *);
     KernT k = threads == 512 ? (KernT)decode_kernel<512, 4, false, false>
             : threads == 768 ? (KernT)decode_kernel<768, 2, false, false> : (KernT)decode_kernel<640, 2, false, false>;
     int num = 0;
@@ -849,8 +878,26 @@ void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched,
                 max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
 }
 
+// Streaming host ring of a refilling decode (lb_decode_batch, large 1-best batches).
+struct RingDev {
+    const int *ready;
+    int *done;
+    const double *base;
+    long long slot_doubles;
+    int slots;
+};
+
+// Queue order of a refilling decode: longest first, ties in input order (LPT).
+std::vector<int32_t> lpt_order(int n, const int32_t *T) {
+    std::vector<int32_t> ord(n);
+    for (int u = 0; u < n; u++) ord[u] = u;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return T[x] > T[y]; });
+    return ord;
+}
+
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
-                const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr) {
+                const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr,
+                const RingDev *ring = nullptr) {
     const bool lat = cfg->want_lattice != 0;
     if (lat) {
         // size the arena for what the last lattice decode took, so a steady
@@ -938,6 +985,13 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     p.exp = ex ? atoi(ex) : 0;
     p.ready = d_ready;
     if (batched && d_ready) return set_err(LB_INTERNAL, "progressive staging needs the lane kernel");
+    if (ring) {
+        p.ring_ready = ring->ready;
+        p.ring_done = ring->done;
+        p.ring_base = ring->base;
+        p.ring_slot_doubles = ring->slot_doubles;
+        p.ring_slots = ring->slots;
+    }
     const char *pe = getenv("LB_PHASE_PROFILE");
     unsigned long long *d_prof = nullptr;
     if (pe && pe[0] == '1') {
@@ -947,13 +1001,13 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     }
     const size_t smem = lane_dyn_smem(threads, D, p.acrow_smem != 0);
     // decode-lane variants: CTA size x batch width x lattice x phase-profile
-    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, int);
+    using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, const UttJob *, int, int *);
     const bool prof = p.prof != nullptr;
 #define LB_PICK(NT, U)                                                                     \
     (lat ? (prof ? decode_kernel<NT, U, true, true> : decode_kernel<NT, U, true, false>) \
          : (prof ? decode_kernel<NT, U, false, true> : decode_kernel<NT, U, false, false>))
     KernT kern;
-// 640 threads (96 registers, few spills) measured best on C4: 440k vs 392k
+    // 640 threads (96 registers, few spills) measured best on C4: 440k vs 392k
     // frames/s at 768 and 417k at 512 (tools/cta_sweep.sh)
     if (threads == 640) kern = LB_PICK(640, 2);
     else if (threads == 768) kern = LB_PICK(768, 2);
@@ -962,6 +1016,38 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
 #undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     const GraphDev gd = g->dev();
+
+    // Per-utterance output slots (status, costs, counters, best path) for the
+    // whole call, so lanes that refill from the job queue keep every result.
+    const int pstride = path_cap;
+    if (int rj = ensure_jobs(w, n, pstride)) return rj;
+    std::vector<UttJob> hj(n);
+    for (int u = 0; u < n; u++) {
+        UttJob &J = hj[u];
+        std::memset(&J, 0, sizeof(J));
+        J.costs = dev_costs[u];
+        J.T = T[u];
+        J.path = w.j_path + (size_t)u * pstride;
+        J.out_i = w.j_out_i + 8 * (size_t)u;
+        J.out_d = w.j_out_d + 4 * (size_t)u;
+        J.out_c = w.j_out_c + 8 * (size_t)u;
+    }
+    // Refilling lanes (1-best in the persistent-lane kernel): ONE launch for the
+    // whole call; lanes claim jobs longest first from a device counter, so a
+    // ragged batch never waits for a wave's longest utterance.  Lattice and
+    // token-list decodes keep their per-utterance arenas until readback, so they
+    // run in waves of `lanes` utterances (the wave's lane l decodes job l).
+    const bool refill = !batched && !lat && !packs && d_ready == nullptr && !getenv("LB_NO_REFILL");
+    if (ring && !(refill && p.acrow_smem)) return set_err(LB_INTERNAL, "streamed staging needs refilling lanes");
+    std::vector<UttJob> jq(n);
+    if (refill) {
+        const std::vector<int32_t> ord = lpt_order(n, T);
+        for (int k = 0; k < n; k++) jq[k] = hj[ord[k]];
+    } else {
+        jq = hj;
+    }
+    CK(cudaMemcpyAsync(w.d_jobs, jq.data(), (size_t)n * sizeof(UttJob), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w.j_out_i, 0, 8 * sizeof(int) * (size_t)std::max(n, 1), st));
 
     cudaEvent_t e0, e1, e2, e3;
     CK(cudaEventCreate(&e0));
@@ -972,18 +1058,28 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     res->t_h2d = h2d_ms;
     FlScratch &fl = g->fl;
     std::vector<UttDesc> desc(lanes);
-    std::vector<int> hi(8 * lanes);
-    std::vector<double> hd(4 * lanes);
-    std::vector<long long> hc(8 * lanes);
-    // best paths are laid out at the workspace's stride (slot_desc), which can be
-    // larger than this call's path_cap when an earlier call grew the workspace
-    const size_t pstride = (size_t)w.path_cap;
-    std::vector<int> hpath(pstride * lanes);
-    for (int w0 = 0; w0 < n; w0 += lanes) {
-        const int nw = std::min(lanes, n - w0);
-        for (int l = 0; l < nw; l++) desc[l] = slot_desc(w, l, dev_costs[w0 + l], T[w0 + l], tok_cap, lat_cap);
+    std::vector<int> hi(8 * (size_t)std::max(n, 1));
+    std::vector<double> hd(4 * (size_t)std::max(n, 1));
+    std::vector<long long> hc(8 * (size_t)std::max(n, 1));
+    std::vector<int> hpath((size_t)pstride * std::max(n, 1));
+    const int step = refill ? n : lanes;
+    for (int w0 = 0; w0 < n; w0 += step) {
+        const int nw = refill ? std::min(lanes, n) : std::min(lanes, n - w0);   // lanes launched
+        const int nj = refill ? n : nw;                                          // jobs of the launch
+        for (int l = 0; l < nw; l++) {
+            desc[l] = slot_desc(w, l, nullptr, 0, tok_cap, lat_cap);
+            desc[l].path_cap = pstride;   // the job path slots' stride (ensure_jobs)
+            if (!refill) {   // the wave's job l (the prune kernel and finaliser read these)
+                desc[l].costs = dev_costs[w0 + l];
+                desc[l].T = T[w0 + l];
+                desc[l].path = hj[w0 + l].path;
+                desc[l].out_i = hj[w0 + l].out_i;
+                desc[l].out_d = hj[w0 + l].out_d;
+                desc[l].out_c = hj[w0 + l].out_c;
+            }
+        }
         CK(cudaMemcpyAsync(w.d_desc, desc.data(), nw * sizeof(UttDesc), cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(w.out_i, 0, 8 * sizeof(int) * nw, st));
+        if (refill) CK(cudaMemsetAsync(w.queue, 0, sizeof(int), st));
         CK(cudaEventRecord(e0, st));
         if (batched) {
             int rcb = launch_batched(g, gd, p, w, nw, T + w0, bpl, st, res);
@@ -1001,7 +1097,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc, nw));
+            CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc,
+                                  (const UttJob *)(w.d_jobs + (refill ? 0 : w0)), nj, refill ? w.queue : nullptr));
             res->launches++;
         }
         CK(cudaEventRecord(e1, st));
@@ -1023,10 +1120,15 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             res->launches++;
         }
         CK(cudaEventRecord(e2, st));
-        CK(cudaMemcpyAsync(hi.data(), w.out_i, 8 * sizeof(int) * nw, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hd.data(), w.out_d, 4 * sizeof(double) * nw, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hc.data(), w.out_c, 8 * sizeof(long long) * nw, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hpath.data(), w.path, sizeof(int) * pstride * nw, cudaMemcpyDeviceToHost, st));
+        const int u0 = refill ? 0 : w0;
+        CK(cudaMemcpyAsync(hi.data() + 8 * (size_t)u0, w.j_out_i + 8 * (size_t)u0, 8 * sizeof(int) * (size_t)nj,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hd.data() + 4 * (size_t)u0, w.j_out_d + 4 * (size_t)u0, 4 * sizeof(double) * (size_t)nj,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hc.data() + 8 * (size_t)u0, w.j_out_c + 8 * (size_t)u0, 8 * sizeof(long long) * (size_t)nj,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hpath.data() + (size_t)pstride * u0, w.j_path + (size_t)pstride * u0,
+                           sizeof(int) * (size_t)pstride * nj, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -1034,27 +1136,30 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaEventElapsedTime(&ms, e1, e2));
         res->t_prune += ms;
         CK(cudaEventRecord(e2, st));
-        for (int l = 0; l < nw; l++) {
-            UttHost &u = res->utts[w0 + l];
-            const int code = hi[8 * l + 0];
-            std::memcpy(u.counters, &hc[8 * l], sizeof(u.counters));
+        for (int k = 0; k < nj; k++) {
+            const int uu = u0 + k;
+            UttHost &u = res->utts[uu];
+            const int code = hi[8 * (size_t)uu + 0];
+            std::memcpy(u.counters, &hc[8 * (size_t)uu], sizeof(u.counters));
             if (code != E_OK) {
-                fill_message(u, code, hi[8 * l + 1], hd[4 * l + 2], *cfg);
+                fill_message(u, code, hi[8 * (size_t)uu + 1], hd[4 * (size_t)uu + 2], *cfg);
                 continue;
             }
             u.status = LB_OK;
-            u.partial = hi[8 * l + 2];
-            u.total_cost = hd[4 * l + 0];
-            const int plen = hi[8 * l + 4];
-            if (plen < 0 || (size_t)plen > pstride) return set_err(LB_INTERNAL, "best path length out of range");
-            u.path.assign(hpath.begin() + pstride * l, hpath.begin() + pstride * l + plen);
+            u.partial = hi[8 * (size_t)uu + 2];
+            u.total_cost = hd[4 * (size_t)uu + 0];
+            const int plen = hi[8 * (size_t)uu + 4];
+            if (plen < 0 || plen > pstride) return set_err(LB_INTERNAL, "best path length out of range");
+            u.path.assign(hpath.begin() + (size_t)pstride * uu, hpath.begin() + (size_t)pstride * uu + plen);
+            if (refill) continue;
+            const int l = k;
             if (lat) {
-                rc = finalize_device(g, desc[l], T[w0 + l], D, cfg->acoustic_scale, cfg->lattice_beam, u.partial, fl,
-                                     st, u, n - (w0 + l));
+                rc = finalize_device(g, desc[l], T[uu], D, cfg->acoustic_scale, cfg->lattice_beam, u.partial, fl,
+                                     st, u, n - uu);
                 if (rc) return rc;
             }
             if (packs || keep_work) {
-                const int Tu = T[w0 + l];
+                const int Tu = T[uu];
                 const UttDesc &d = desc[l];
                 u.frame_off.resize(Tu + 2);
                 CK(cudaMemcpy(u.frame_off.data(), d.tok_base, sizeof(long long) * (Tu + 2), cudaMemcpyDeviceToHost));
@@ -1109,6 +1214,92 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         cudaFree(d_prof);
     }
     return guard_round_tags(w, st);
+}
+
+// Streamed host input for a refilling decode: job k (LPT queue order) is copied
+// into slot k % R of a mapped pinned ring by host threads and published in
+// order through a mapped counter (Params::ring_ready); a lane that finishes job
+// j hands its slot back (ring_done[slot] = j + 1) and the host reuses it for
+// job j + R.  Host memory stays bounded (R slots) and the copy overlaps the
+// decode instead of preceding it (pinned buffering of the
+// log-likelihood H2D).
+int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T, int D, const lb_config *cfg,
+                int lanes, lb_result *res) {
+    int tmax = 1;
+    for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
+    const long long slot_doubles = ((long long)tmax * D + 15) & ~15ll;   // slots start on 128-byte lines
+    int R = std::min(n, std::max(2 * lanes, lanes + 8));
+    if (const char *e = getenv("LB_RING_SLOTS")) R = std::max(1, std::min(n, atoi(e)));
+    const size_t need = (size_t)R * slot_doubles * 8;
+    if (need > g->ring_cap) {
+        if (g->ring) cudaFreeHost(g->ring);
+        g->ring = nullptr;
+        g->ring_cap = 0;
+        CK(cudaHostAlloc((void **)&g->ring, need, cudaHostAllocMapped));
+        g->ring_cap = need;
+    }
+    if (R + 1 > g->ring_ctl_cap) {
+        if (g->ring_ctl) cudaFreeHost(g->ring_ctl);
+        g->ring_ctl = nullptr;
+        g->ring_ctl_cap = 0;
+        CK(cudaHostAlloc((void **)&g->ring_ctl, sizeof(int) * (size_t)(R + 32), cudaHostAllocMapped));
+        g->ring_ctl_cap = R + 32;
+    }
+    int *h_ready = g->ring_ctl, *h_done = g->ring_ctl + 32;   // ready on its own line
+    __atomic_store_n(h_ready, 0, __ATOMIC_SEQ_CST);
+    for (int k = 0; k < R; k++) __atomic_store_n(h_done + k, 0, __ATOMIC_SEQ_CST);
+    RingDev rd;
+    CK(cudaHostGetDevicePointer((void **)&rd.ready, h_ready, 0));
+    CK(cudaHostGetDevicePointer((void **)&rd.done, h_done, 0));
+    CK(cudaHostGetDevicePointer((void **)&rd.base, g->ring, 0));
+    rd.slot_doubles = slot_doubles;
+    rd.slots = R;
+    const std::vector<int32_t> ord = lpt_order(n, T);
+    unsigned nth = std::max(1u, std::min(4u, std::thread::hardware_concurrency()));
+    if (const char *se = getenv("LB_STAGE_THREADS")) nth = std::max(1, atoi(se));
+    nth = std::min<unsigned>(nth, (unsigned)n);
+    std::unique_ptr<std::atomic<int>[]> staged(new std::atomic<int>[n]);
+    for (int k = 0; k < n; k++) staged[k].store(0);
+    std::atomic<int> pub{0};
+    std::atomic<bool> abort_flag{false};
+    char *ring = reinterpret_cast<char *>(g->ring);
+    auto publish = [&]() {   // advance the in-order published count as far as staged jobs allow
+        int r = pub.load(std::memory_order_acquire);
+        while (r < n && staged[r].load(std::memory_order_acquire)) {
+            if (pub.compare_exchange_weak(r, r + 1, std::memory_order_acq_rel)) {
+                int cur = __atomic_load_n(h_ready, __ATOMIC_ACQUIRE);
+                while (cur < r + 1 &&
+                       !__atomic_compare_exchange_n(h_ready, &cur, r + 1, false, __ATOMIC_RELEASE, __ATOMIC_ACQUIRE)) {
+                }
+                r = r + 1;
+            }
+        }
+    };
+    auto work = [&](unsigned t) {
+        for (int k = (int)t; k < n; k += (int)nth) {
+            const int slot = k % R;
+            if (k >= R) {   // wait for the slot's previous job (k - R) to hand it back
+                int spins = 0;
+                while (__atomic_load_n(h_done + slot, __ATOMIC_ACQUIRE) < k - R + 1) {
+                    if (abort_flag.load(std::memory_order_relaxed)) return;
+                    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+                }
+            }
+            std::memcpy(ring + (size_t)slot * slot_doubles * 8, costs[ord[k]], (size_t)T[ord[k]] * D * 8);
+            staged[k].store(1, std::memory_order_release);
+            publish();
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nth; t++) th.emplace_back(work, t);
+    const int rc = decode_impl(g, n, costs, T, D, cfg, g->stream, res, 0.0f, nullptr, &rd);
+    // a kernel that ran to the end consumed every job, so the stagers are done;
+    // after a failure they may wait on a slot that is never handed back
+    abort_flag.store(true);
+    for (auto &x : th) x.join();
+    res->t_h2d = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
 }
 
 }  // namespace
@@ -1286,6 +1477,8 @@ int lb_graph_destroy(lb_graph *g) {
     cudaFree(g->d_costs);
     if (g->h_stage) cudaFreeHost(g->h_stage);
     if (g->h_ready) cudaFreeHost(g->h_ready);
+    if (g->ring) cudaFreeHost(g->ring);
+    if (g->ring_ctl) cudaFreeHost(g->ring_ctl);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
     return LB_OK;
@@ -1313,12 +1506,6 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     std::lock_guard<std::mutex> lock(g->mu);
     CK(cudaSetDevice(g->device));
     std::unique_ptr<lb_result> res(new lb_result());
-    if (total > g->h_stage_cap) {
-        if (g->h_stage) cudaFreeHost(g->h_stage);
-        g->h_stage = nullptr;
-        CK(cudaHostAlloc((void **)&g->h_stage, std::max<size_t>(total, 1) * 8, cudaHostAllocMapped));
-        g->h_stage_cap = total;
-    }
     // 1-best decodes in the lane kernel read each frame's row once per lane: the
     // kernel reads the mapped staging buffer directly (zero-copy).  Lattice decodes
     // re-read rows in the prune pass, and the batched mode gathers acoustic costs
@@ -1329,6 +1516,22 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     const bool lane_mode = !batched_mode;
     const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
                            !getenv("LB_E2E_COPY");
+    // Batches larger than one set of lanes refill lanes from the job queue; their
+    // rows stream through a bounded pinned ring instead of a whole-batch stage.
+    const int lanes_est = cfg->lanes > 0 ? cfg->lanes : std::max(1, g->sms / std::max(lane_c, 1));
+    if (zero_copy && n > lanes_est && !cfg->collect_frame_packs && !getenv("LB_NO_RING") &&
+        !getenv("LB_NO_REFILL")) {
+        rc = decode_ring(g, n, costs, T, D, cfg, lanes_est, res.get());
+        if (rc) return rc;
+        *out = res.release();
+        return LB_OK;
+    }
+    if (total > g->h_stage_cap) {
+        if (g->h_stage) cudaFreeHost(g->h_stage);
+        g->h_stage = nullptr;
+        CK(cudaHostAlloc((void **)&g->h_stage, std::max<size_t>(total, 1) * 8, cudaHostAllocMapped));
+        g->h_stage_cap = total;
+    }
     // Stage the caller's matrices into pinned, device-mapped memory with all host
     // threads (one memcpy thread is ~10 GB/s).  Zero-copy decodes stage
     // progressively: frame chunks of every utterance in order, each published
@@ -1894,7 +2097,12 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
         CK(dalloc(&d_row, D));
         CK(cudaMemcpyAsync(d_row, acrow, 8 * (size_t)D, cudaMemcpyHostToDevice, st));
     }
+    if (int rj = ensure_jobs(w, 1, 16)) return rj;
     UttDesc d = slot_desc(w, 0, d_row, 1);
+    d.path = w.j_path;
+    d.out_i = w.j_out_i;
+    d.out_d = w.j_out_d;
+    d.out_c = w.j_out_c;
     std::vector<unsigned> hs(states, states + n);
     CK(cudaMemcpyAsync(d.tok_state, hs.data(), 4 * n, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.tok_cost, costs, 8 * n, cudaMemcpyHostToDevice, st));

@@ -244,6 +244,18 @@ struct UttDesc {
     long long *out_c;       // counters[8]
 };
 
+// One utterance of a decode call: its cost matrix, length and output slots
+// (per job, so lanes that refill from the job queue keep every job's result).
+struct UttJob {
+    const double *costs;    // T x D f64 (device or mapped host)
+    int T;
+    int _pad;
+    int *path;              // [path_cap] best path arcs
+    int *out_i;             // [8] status, err_frame, partial, best_idx, path_len, n_frames_done
+    double *out_d;          // [4] total_cost, best_total, err_aux
+    long long *out_c;       // [8] counters
+};
+
 struct Params {
     double beam, lattice_beam, scale;
     long long max_active, max_tokens;
@@ -255,6 +267,16 @@ struct Params {
     int exp;                    // timing experiments (LB_EXP, profiling only; results not exact)
     const int *ready;           // progressive host staging (mapped): rows of frames < *ready are
                                 // in place for every utterance; nullptr = all rows ready
+    // Streaming host staging for refilling lanes (mapped pinned ring of
+    // ring_slots slots; job j, in queue order, lives in slot j % ring_slots):
+    // the host publishes *ring_ready = jobs staged so far, in order; a lane
+    // marks ring_done[slot] = j + 1 once job j's rows are no longer needed.
+    const int *ring_ready;      // nullptr = no ring (costs per job)
+    int *ring_done;
+    const double *ring_base;
+    long long ring_slot_doubles;
+    int ring_slots;
+    int _pad2;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -341,8 +341,8 @@ struct Lane {
 
     __device__ void load_row(const double *r, int frame) {
         row = r;
-        if (p.ready) {
-            wait_rows(frame + 1);
+        if (p.ready || p.ring_ready) {
+            if (p.ready) wait_rows(frame + 1);
             // L2-only loads (ld.cg): a published row was never cached before it was
             // written (the host aligns chunks to 128-byte lines); ld.cv would be
             // safe without that but costs ~130 us per frame on mapped memory.
@@ -1027,27 +1027,15 @@ __device__ __forceinline__ void seed_start(Lane<UNR> &ln, const GraphDev &g, con
 }
 
 // ===========================================================================
-// Full-utterance decode: one cluster (lane) per utterance of the wave.
-// Cluster barriers per frame: emit 1, winners 1, epsilon 1 per round,
-// aggregate 1-2, lattice 1.
+// Full-utterance decode of one job on one lane (a cluster).  Cluster barriers
+// per frame: emit 1, winners 1, epsilon 1 per round, aggregate 1-2, lattice 1.
+// `io` is the CTA's shared-memory descriptor of the job: the lane's arenas plus
+// the job's costs, length and output slots.
 // ===========================================================================
-template <int NT, int UNR, bool LAT, bool PROF>
-__global__ void __launch_bounds__(NT, 1)
-decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
-              const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ utts, int n_utts) {
+template <int UNR, bool LAT, bool PROF>
+__device__ __forceinline__ void decode_one(const GraphDev &g, const Params &p, const LaneWs &L,
+                                           const UttDesc &io, const Grp &G) {
     Smem &sm = lane_sm;
-    cgx::cluster_group cl = cgx::this_cluster();
-    Grp G;
-    G.C = (int)cl.num_blocks();
-    G.rank = (int)cl.block_rank();
-    G.M = cl.map_shared_rank(&sm, 0);
-    const int u_idx = blockIdx.x / G.C;      // uniform across the cluster
-    if (u_idx >= n_utts) return;
-    const LaneWs &L = lanes[u_idx];
-    const UttDesc &io = utts[u_idx];
-    init_smem(__ldcg(L.round_ctr));
-    G.sync();
-
     Lane<UNR> ln(g, p, L, io, G, lane_dyn);
     if (PROF) ln.wprof = p.prof + 8;
     const int T = io.T;
@@ -1065,7 +1053,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         }
     };
     mark(-1);
-
     double beam_eff = p.beam;   // adaptive beam; == beam without max-active
 
     // ---- frame 0 (decoder.py:510-523): start token, epsilon closure ----
@@ -1188,7 +1175,6 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         io.out_c[5] = (long long)cec;
         io.out_c[6] = (long long)sm.c_next;
         io.out_c[7] = lb;
-        __stcg(L.round_ctr, sm.round_id);
         io.out_i[5] = tdone;
     }
     const int err = G.M->err;
@@ -1251,6 +1237,93 @@ decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         io.out_i[1] = e ? f : 0;
     }
     mark(7);
+    G.sync();
+}
+
+// Per-CTA shared copy of the current job's descriptor (lane arenas + job fields).
+__shared__ UttDesc lane_io;
+__shared__ int lane_job;
+
+// ===========================================================================
+// Persistent decode lanes: one cluster per lane.  With a queue, a lane claims
+// jobs from the device counter (jobs are in longest-first order, the host's
+// LPT sort) and refills itself the moment it finishes one, as the reference's
+// decode_batch pool starts the next utterance when a worker frees up
+// (decoder.py:666-672); without one, lane l decodes job l (lattice waves).
+// ===========================================================================
+template <int NT, int UNR, bool LAT, bool PROF>
+__global__ void __launch_bounds__(NT, 1)
+decode_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params p,
+              const LaneWs *__restrict__ lanes, const UttDesc *__restrict__ slots,
+              const UttJob *__restrict__ jobs, int n_jobs, int *queue) {
+    Smem &sm = lane_sm;
+    cgx::cluster_group cl = cgx::this_cluster();
+    Grp G;
+    G.C = (int)cl.num_blocks();
+    G.rank = (int)cl.block_rank();
+    G.M = cl.map_shared_rank(&sm, 0);
+    const int lane = blockIdx.x / G.C;      // uniform across the cluster
+    const LaneWs &L = lanes[lane];
+    unsigned round_id = __ldcg(L.round_ctr);
+    int ready_seen = 0;
+    for (int it = 0;; it++) {
+        if (queue) {
+            if (G.leader()) lane_job = atomicAdd(queue, 1);
+            G.sync();
+            const int j = *cl.map_shared_rank(&lane_job, 0);
+            G.sync();   // every CTA has read the claim before the next one
+            if (threadIdx.x == 0) lane_job = j;
+        } else if (threadIdx.x == 0) {
+            lane_job = it == 0 ? lane : n_jobs;
+        }
+        __syncthreads();
+        const int j = lane_job;
+        if (j >= n_jobs) break;
+        if (p.ring_ready) {   // streamed host rows: wait until job j is staged
+            if (threadIdx.x == 0) {
+                int r;
+                for (;;) {
+                    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(r) : "l"(p.ring_ready) : "memory");
+                    if (r > j) break;
+                    __nanosleep(2000);
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            UttDesc d = slots[lane];
+            const UttJob &J = jobs[j];
+            d.costs = p.ring_ready ? p.ring_base + (long long)(j % p.ring_slots) * p.ring_slot_doubles : J.costs;
+            d.T = J.T;
+            d.path = J.path;
+            d.out_i = J.out_i;
+            d.out_d = J.out_d;
+            d.out_c = J.out_c;
+            lane_io = d;
+            init_smem(round_id);
+            sm.ready_seen = ready_seen;
+        }
+        G.sync();
+        decode_one<UNR, LAT, PROF>(g, p, L, lane_io, G);
+        round_id = sm.round_id;
+        ready_seen = sm.ready_seen;
+        if (p.ring_ready) {
+            // Hand the slot back: drop its lines from L2 (the host rewrites the
+            // slot for job j + ring_slots, and a stale line must not survive),
+            // then publish with a system-scope release.
+            const char *base = reinterpret_cast<const char *>(lane_io.costs);
+            const long long lines = ((long long)lane_io.T * p.D * 8 + 127) / 128;
+            for (long long q = G.gtid(); q < lines; q += G.gstride())
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + q * 128) : "memory");
+            G.sync();
+            if (G.leader()) {
+                asm volatile("fence.sc.sys;" ::: "memory");
+                asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p.ring_done + (j % p.ring_slots)), "r"(j + 1)
+                             : "memory");
+            }
+        }
+    }
+    if (G.leader()) __stcg(L.round_ctr, round_id);
     G.sync();   // keep rank 0's shared memory alive until every CTA is done with it
 }
 

@@ -190,6 +190,25 @@ def device_replicas(wfst, devices) -> list:
     return out
 
 
+def split_batch(lengths, n_shards: int) -> list:
+    """Input indices of each shard under shard_lpt, ascending within a shard."""
+    sh = shard_lpt(lengths, n_shards)
+    return [np.flatnonzero(sh == k).tolist() for k in range(int(n_shards))]
+
+
+def merge_in_order(n: int, shards: list, shard_results: list) -> list:
+    """Inverse of split_batch: per-shard result lists back into input order."""
+    out = [None] * int(n)
+    for idx, res in zip(shards, shard_results):
+        if len(idx) != len(res):
+            raise UsageError("shard result count does not match its utterances")
+        for i, r in zip(idx, res):
+            out[i] = r
+    if any(r is None for r in out) and n:
+        raise UsageError("shards do not cover the batch")
+    return out
+
+
 def shard_lpt(lengths, n_shards: int) -> np.ndarray:
     """The longest-first utterance split the multi-device decode uses
     (lb_shard_lpt): shard index per utterance."""

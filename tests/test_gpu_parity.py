@@ -448,3 +448,74 @@ def test_epsilon_round_tags_reset(oracle_mod, monkeypatch):
         res = lb.decode_batch(w, mats, cfg, want_lattice=False)
         tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
         assert all(st == 0) and [r.total_cost for r in res] == tc.tolist()
+
+
+def _ragged_batch(n, seed0, num_pdfs=300, tmin=8, tmax=70):
+    rng = np.random.default_rng(seed0)
+    return [np.ascontiguousarray(synthetic.hclg_matrix(seed0 + i, num_frames=int(rng.integers(tmin, tmax + 1)),
+                                                       num_pdfs=num_pdfs).costs) for i in range(n)]
+
+
+@pytest.mark.parametrize("slots", [0, 1, 3])
+def test_refilling_lanes_streamed_ring(oracle_mod, monkeypatch, slots):
+    """A ragged batch much larger than the lane count: one launch, lanes refill
+    from the longest-first job queue, host rows stream through the pinned ring
+    (LB_RING_SLOTS forces heavy slot reuse: every slot is rewritten many times
+    inside one kernel).  Every utterance equals the oracle, in input order."""
+    if slots:
+        monkeypatch.setenv("LB_RING_SLOTS", str(slots))
+    w = synthetic.hclg_graph(9, num_states=60_000, pool_size=1500, num_pdfs=300)
+    mats = _ragged_batch(90, 7000 + slots)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=6)
+    res = lb.decode_batch(w, mats, cfg, want_lattice=False)
+    tc, st, cnt = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()
+    assert [[r.counters["n_tokens"], r.counters["n_scan"], r.counters["n_next"]] for r in res] == \
+        [[c[0], c[1], c[6]] for c in cnt]
+    for i in (0, 17, 89):
+        ref = oracle_mod.decode(w, mats[i], 12.0, max_active=600, want_lattice=False, collect_frames=False)
+        assert res[i].words == ref.words and res[i].alignment == ref.alignment
+
+
+def test_refilling_lanes_device_resident(oracle_mod):
+    """The same queue with HBM-resident costs (lb_decode_batch_device)."""
+    import torch
+
+    from paper_1804_03243_b200.resident import decode_batch_resident
+    w = synthetic.hclg_graph(9, num_states=60_000, pool_size=1500, num_pdfs=300)
+    mats = _ragged_batch(70, 7100)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=5)
+    outs, _ = decode_batch_resident(w, [torch.from_numpy(m.copy()).cuda() for m in mats], cfg)
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
+    assert all(st == 0) and [o["total_cost"] for o in outs] == tc.tolist()
+    assert all(o["status"] == 0 for o in outs)
+
+
+def test_refill_and_waves_agree(monkeypatch):
+    """Refilling lanes (default) and static waves (LB_NO_REFILL) give identical results."""
+    w = synthetic.hclg_graph(10, num_states=60_000, pool_size=1500, num_pdfs=300)
+    mats = _ragged_batch(40, 7200)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=4)
+    a = lb.decode_batch(w, mats, cfg, want_lattice=False)
+    monkeypatch.setenv("LB_NO_REFILL", "1")
+    b = lb.decode_batch(w, mats, cfg, want_lattice=False)
+    assert [(r.total_cost, r.words, r.alignment) for r in a] == [(r.total_cost, r.words, r.alignment) for r in b]
+
+
+def test_multi_device_replicas_on_one_gpu(oracle_mod):
+    """decode_batch(devices=[0, 0]): two independent replicas of the graph on
+    device 0, LPT shards on two host threads (lb_decode_batch_multi), results in
+    input order equal to the single-replica decode and the oracle."""
+    w = synthetic.hclg_graph(11, num_states=60_000, pool_size=1500, num_pdfs=300)
+    mats = _ragged_batch(30, 7300)
+    one = lb.decode_batch(w, mats, lb.DecodeConfig(beam=12.0, max_active=600), want_lattice=False)
+    two = lb.decode_batch(w, mats, lb.DecodeConfig(beam=12.0, max_active=600, devices=(0, 0)),
+                          want_lattice=False)
+    assert [(r.total_cost, r.words) for r in one] == [(r.total_cost, r.words) for r in two]
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
+    assert [r.total_cost for r in two] == tc.tolist()
+    lat = lb.decode_batch(w, mats[:6], lb.DecodeConfig(beam=12.0, lattice_beam=4.0, max_active=600,
+                                                       devices=(0, 0)))
+    single = lb.decode_batch(w, mats[:6], lb.DecodeConfig(beam=12.0, lattice_beam=4.0, max_active=600))
+    assert all(a.lattice.same_lattice(b.lattice) for a, b in zip(lat, single))
