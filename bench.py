@@ -64,6 +64,12 @@ def exp_bytes_of(c):
     return 28 * c[0] + 16 * c[1] + 8 * c[2]
 
 
+def _jsonable(o):
+    if isinstance(o, np.generic):
+        return o.item()
+    raise TypeError(f"not JSON serialisable: {type(o).__name__}")
+
+
 def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -266,7 +272,7 @@ def run_reference(args, dist: Dist):
            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
                             "sample": sample},
            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out, default=_jsonable), flush=True)
     dist.close()
 
 
@@ -491,7 +497,7 @@ def main(argv=None):
                "arcs_per_sec": arcs_all / (t_max / 1e3),
                "config": config_dict(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "clocks": ck, "ragged_variant": ragged, "configs_measured": configs}
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out, default=_jsonable), flush=True)
     dist.close()
 
 

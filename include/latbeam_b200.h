@@ -169,6 +169,22 @@ int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const
                         const int64_t *ilabel, const int64_t *olabel, const double *graph_cost,
                         const double *acoustic_cost, char *buf, int64_t cap);
 
+/* prune_lattice (lattice.py:365-431) of a work lattice handed in by the caller,
+ * on the device.  Frames 0..t: frame_off[t+2] offsets into fwd (each frame's
+ * token forward costs); blocks 0..t: block_off[t+2] offsets into the arc
+ * columns.  An arc of block b goes from token from_idx of frame b-1 (emitting
+ * != 0) or b (epsilon) to token to_idx of frame b.  status: 0 LIVE, 1 PRUNED
+ * (pruned arcs stay pruned and do not participate).  terminus = frame t's
+ * extra-cost start (zeros, or totals - min(totals) with final costs).  On
+ * return every LIVE arc carries its extra (extra[]) and is PRUNED when
+ * extra > lattice_beam; node_extra (frame_off[t+1] entries) holds the node
+ * extras.  LB_INTERNAL if an in-frame epsilon fixpoint does not settle. */
+int lb_prune_lattice(int32_t device, int32_t t, const int64_t *frame_off, const double *fwd,
+                     const int64_t *block_off, const int32_t *from_idx, const int32_t *to_idx,
+                     const uint8_t *emitting, const double *graph_cost, const double *acoustic_cost,
+                     const double *terminus, double lattice_beam, uint8_t *status, double *extra,
+                     double *node_extra);
+
 /* Single-op surfaces (decoder.py:373-435): one frontier on device.
  * out_* need room for num_states entries; *n_out receives the count. */
 int lb_expand_emitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n,

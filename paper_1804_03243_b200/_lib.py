@@ -53,6 +53,8 @@ SIGNATURES = {
     "lb_result_final_arrays64": (C.c_int, [PV, C.c_int32, P64, P64, P64, PD, P64, P64, P64, P64, PD, PD]),
     "lb_lattice_text": (C.c_int64, [C.c_int64, C.c_int64, C.c_int64, P64, PD, C.c_int64, P64, P64, P64,
                                     P64, PD, PD, C.c_char_p, C.c_int64]),
+    "lb_prune_lattice": (C.c_int, [C.c_int32, C.c_int32, P64, PD, P64, P32, P32, C.POINTER(C.c_uint8), PD, PD,
+                                   PD, C.c_double, C.POINTER(C.c_uint8), PD, PD]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,
                                      P64, PD]),
     "lb_expand_nonemitting": (C.c_int, [PV, P32, PD, C.c_int64, C.c_double, P32, PD, P64]),

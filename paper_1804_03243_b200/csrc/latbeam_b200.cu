@@ -2081,6 +2081,104 @@ int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const
     return total;
 }
 
+// prune_lattice (lattice.py:365-431) on the device for a host work lattice.
+int lb_prune_lattice(int32_t device, int32_t t, const int64_t *frame_off, const double *fwd, const int64_t *block_off,
+                     const int32_t *from_idx, const int32_t *to_idx, const uint8_t *emitting, const double *graph_cost,
+                     const double *acoustic_cost, const double *terminus, double lattice_beam, uint8_t *status,
+                     double *extra, double *node_extra) {
+    if (t < 0 || !frame_off || !block_off) return set_err(LB_USAGE, "bad prune arguments");
+    if (!(lattice_beam >= 0)) return set_err(LB_USAGE, "lattice_beam must be >= 0");
+    const int64_t ntok = frame_off[t + 1], narc = block_off[t + 1];
+    if (ntok < 1 || frame_off[t + 1] - frame_off[t] < 1) return set_err(LB_USAGE, "frontier is empty");
+    for (int f = 0; f <= t; f++)
+        if (frame_off[f + 1] < frame_off[f] || block_off[f + 1] < block_off[f])
+            return set_err(LB_USAGE, "frame / block offsets must be non-decreasing");
+    for (int64_t k = 0; k < narc; k++) {   // arc endpoints inside their frames
+        int b = (int)(std::upper_bound(block_off, block_off + t + 2, k) - block_off) - 1;
+        const int fb = emitting[k] ? b - 1 : b;
+        if (fb < 0 || from_idx[k] < 0 || from_idx[k] >= frame_off[fb + 1] - frame_off[fb] || to_idx[k] < 0 ||
+            to_idx[k] >= frame_off[b + 1] - frame_off[b])
+            return set_err(LB_USAGE, "lattice arc endpoint outside its frame");
+    }
+    CK(cudaSetDevice(device));
+    std::vector<void *> bufs;
+    struct Free { std::vector<void *> &b; ~Free() { for (void *p : b) cudaFree(p); } } fr{bufs};
+    auto up = [&](auto **dp, const auto *hp, size_t cnt) -> cudaError_t {
+        cudaError_t e = dalloc(dp, cnt);
+        if (e != cudaSuccess) return e;
+        bufs.push_back((void *)*dp);
+        return hp ? cudaMemcpy(*dp, hp, sizeof(**dp) * cnt, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    PruneOp op;
+    std::memset(&op, 0, sizeof(op));
+    long long *d_tb, *d_lb;
+    double *d_fwd, *d_g, *d_ac, *d_term, *d_extra, *d_ne_out, *d_tmp;
+    int *d_from, *d_to, *d_err;
+    unsigned char *d_emit, *d_status;
+    unsigned long long *d_ne;
+    const size_t nt = (size_t)ntok, na = (size_t)std::max<int64_t>(narc, 1);
+    const int64_t nterm = frame_off[t + 1] - frame_off[t];
+    CK(up(&d_tb, (const long long *)frame_off, (size_t)t + 2));
+    CK(up(&d_lb, (const long long *)block_off, (size_t)t + 2));
+    CK(up(&d_fwd, fwd, nt));
+    CK(up(&d_from, (const int *)from_idx, (size_t)narc));
+    CK(up(&d_to, (const int *)to_idx, (size_t)narc));
+    CK(up(&d_emit, (const unsigned char *)emitting, (size_t)narc));
+    CK(up(&d_g, graph_cost, (size_t)narc));
+    CK(up(&d_ac, acoustic_cost, (size_t)narc));
+    CK(up(&d_term, terminus, (size_t)nterm));
+    CK(up(&d_status, (const unsigned char *)status, (size_t)narc));
+    CK(up(&d_extra, extra, (size_t)narc));
+    CK(up(&d_ne_out, (const double *)nullptr, nt));
+    CK(up(&d_tmp, (const double *)nullptr, na));
+    CK(up(&d_ne, (const unsigned long long *)nullptr, nt));
+    CK(up(&d_err, (const int *)nullptr, 1));
+    CK(cudaMemset(d_err, 0, 4));
+    op.t = t;
+    op.tok_base = d_tb;
+    op.fwd = d_fwd;
+    op.lat_base = d_lb;
+    op.from = d_from;
+    op.to = d_to;
+    op.emit = d_emit;
+    op.g = d_g;
+    op.ac = d_ac;
+    op.terminus = d_term;
+    op.status = d_status;
+    op.extra = d_extra;
+    op.node_extra = d_ne_out;
+    op.tmp = d_tmp;
+    op.ne = d_ne;
+    op.err_out = d_err;
+    op.beam = lattice_beam;
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    cudaLaunchConfig_t lc = {};
+    const unsigned pc = (unsigned)std::max(1, std::min(8, sms));
+    lc.gridDim = dim3(pc);
+    lc.blockDim = dim3(1024);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, prune_op_kernel, op));
+    CK(cudaGetLastError());
+    int herr = 0;
+    CK(cudaMemcpy(&herr, d_err, 4, cudaMemcpyDeviceToHost));
+    if (herr) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "epsilon extra-cost fixpoint did not settle within frame %d", herr - 1);
+        return set_err(LB_INTERNAL, buf);
+    }
+    CK(cudaMemcpy(status, d_status, (size_t)narc, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(extra, d_extra, 8 * (size_t)narc, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(node_extra, d_ne_out, 8 * nt, cudaMemcpyDeviceToHost));
+    return LB_OK;
+}
+
 static int expand_common(lb_graph *g, const int32_t *states, const double *costs, int64_t n, const double *acrow,
                          int32_t D, double beam, double cutoff, int mode, int32_t *out_states, double *out_costs,
                          int64_t *n_out, double *cutoff_out) {

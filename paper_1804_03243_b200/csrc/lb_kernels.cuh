@@ -1456,6 +1456,106 @@ prune_kernel(GraphDev g, Params p, const UttDesc *__restrict__ utts, int n_utts)
 }
 
 // ===========================================================================
+// prune_lattice single-op surface (lattice.py:365-497) over an arbitrary work
+// lattice handed in by the host: frames 0..t of token costs, blocks 0..t of
+// arcs with their status (LIVE 0 / PRUNED 1; pruned arcs stay pruned and do
+// not participate), graph / acoustic costs and an emitting flag.  Same
+// relaxation as prune_kernel (one cluster, backward over frames, 64-bit
+// atomicMin on the order-preserving f64 key, Jacobi in-frame epsilon
+// fixpoint, clamp at 0), from the given terminus; then every LIVE arc of
+// blocks 0..t gets its extra and is flagged PRUNED when extra > lattice_beam.
+// ===========================================================================
+struct PruneOp {
+    int t;
+    int err;                          // out: E_INT_PRUNE_EPS frame + 1, or 0
+    const long long *tok_base;        // [t+2]
+    const double *fwd;                // token forward costs, frames 0..t
+    const long long *lat_base;        // [t+2]
+    const int *from, *to;
+    const unsigned char *emit;
+    const double *g, *ac, *terminus;
+    unsigned char *status;
+    double *extra, *node_extra, *tmp;
+    unsigned long long *ne;
+    int *err_out;
+    double beam;
+};
+
+__global__ void __launch_bounds__(1024, 1) prune_op_kernel(const __grid_constant__ PruneOp op) {
+    __shared__ int s_moved;
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    int *m0 = cl.map_shared_rank(&s_moved, 0);
+    const int tid = rank * blockDim.x + threadIdx.x, bd = C * blockDim.x;
+    const double inf = inf_d();
+    for (int f = op.t; f >= 0; f--) {
+        const long long b0 = op.tok_base[f];
+        const int nfr = (int)(op.tok_base[f + 1] - b0);
+        unsigned long long *ne = op.ne + b0;
+        const double *fwd = op.fwd + b0;
+        for (int i = tid; i < nfr; i += bd) __stcg(ne + i, enc64(f == op.t ? op.terminus[i] : inf));
+        cl.sync();
+        if (f < op.t) {
+            const long long b1 = op.tok_base[f + 1];
+            for (long long k = op.lat_base[f + 1] + tid; k < op.lat_base[f + 2]; k += bd) {
+                if (op.status[k] != 0 || !op.emit[k]) continue;
+                const int from = op.from[k], to = op.to[k];
+                const double c = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(fwd[from], op.g[k]), op.ac[k]),
+                                                     op.fwd[b1 + to]),
+                                           op.node_extra[b1 + to]);
+                atom_min_u64(ne + from, enc64(c));
+            }
+            cl.sync();
+        }
+        const long long k0 = op.lat_base[f], k1 = op.lat_base[f + 1];
+        for (int it = 0;; it++) {
+            if (rank == 0 && threadIdx.x == 0) s_moved = 0;
+            cl.sync();
+            for (long long k = k0 + tid; k < k1; k += bd) {
+                if (op.status[k] != 0 || op.emit[k]) continue;
+                const int from = op.from[k], to = op.to[k];
+                const double base = __dsub_rn(__dadd_rn(fwd[from], op.g[k]), fwd[to]);
+                const double c = __dadd_rn(base, dec64(__ldcg(ne + to)));
+                const double before = dec64(__ldcg(ne + from));
+                __stcg(op.tmp + k, c);
+                if (__dsub_rn(before, c) > CONVERGE_TOL) *m0 = 1;
+            }
+            cl.sync();
+            for (long long k = k0 + tid; k < k1; k += bd) {
+                if (op.status[k] != 0 || op.emit[k]) continue;
+                atom_min_u64(ne + op.from[k], enc64(__ldcg(op.tmp + k)));
+            }
+            cl.sync();
+            const int moved = *m0;
+            cl.sync();
+            if (!moved) break;
+            if (it >= nfr) {
+                if (tid == 0) *op.err_out = f + 1;
+                return;
+            }
+        }
+        for (int i = tid; i < nfr; i += bd) {
+            const double x = dec64(__ldcg(ne + i));
+            __stcg(op.node_extra + b0 + i, x < 0.0 ? 0.0 : x);
+        }
+        cl.sync();
+    }
+    const long long nl = op.lat_base[op.t + 1];
+    for (long long k = tid; k < nl; k += bd) {
+        if (op.status[k] != 0) continue;
+        const int b = upper_block(op.lat_base, op.t + 2, k);
+        const long long tbb = op.tok_base[b];
+        const long long fb = op.emit[k] ? op.tok_base[b - 1] : tbb;
+        const double x = __dadd_rn(__dsub_rn(__dadd_rn(__dadd_rn(op.fwd[fb + op.from[k]], op.g[k]), op.ac[k]),
+                                             op.fwd[tbb + op.to[k]]),
+                                   op.node_extra[tbb + op.to[k]]);
+        const double e = x < 0.0 ? 0.0 : x;
+        op.extra[k] = e;
+        if (e > op.beam) op.status[k] = 1;
+    }
+}
+
+// ===========================================================================
 // Single-op surfaces (decoder.py:373-435), one CTA (a cluster of one).
 //   mode 0 = expand_emitting: tokens at io.tok_*[0..n); acrow (scaled) at
 //            io.costs; writes winners <= cutoff to io.tok_state/tok_cost[n ...].

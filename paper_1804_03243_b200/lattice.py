@@ -166,6 +166,73 @@ class WorkLattice:
                 for i in range(len(t["slots"]))]
 
 
+def prune_lattice(lat: WorkLattice, frontier: FrameTokens, lattice_beam: float,
+                  final_costs: np.ndarray | None = None, device: int = 0) -> None:
+    """Flag arcs whose extra cost exceeds lattice_beam (lattice.py:365-431 of
+    `latbeam`), on the device (C-ABI lb_prune_lattice, csrc `prune_op_kernel`).
+
+    Node extras start at the frontier (zeros, or totals - min(totals) when
+    final_costs is given) and relax backward frame by frame with an in-frame
+    epsilon fixpoint; an arc's extra is fwd(from) + graph + acoustic - fwd(to) +
+    node_extra(to), clamped at 0.  LIVE arcs of blocks 0..t get their extra and
+    turn PRUNED when it exceeds lattice_beam; already-pruned arcs stay pruned and
+    do not participate.  Mutates `lat` (block extras / statuses, node_extra)."""
+    import ctypes as C
+
+    from . import _lib
+    from .errors import InternalInvariantError, UsageError
+    if not lattice_beam >= 0:
+        raise UsageError("lattice_beam must be >= 0")
+    t = frontier.frame
+    if not (0 <= t < len(lat.frames)) or lat.frames[t] is not frontier:
+        raise UsageError("frontier is not a frame of this lattice")
+    if frontier.n == 0:
+        raise UsageError("frontier is empty")
+    if final_costs is None:
+        terminus = np.zeros(frontier.n)
+    else:
+        totals = frontier.costs + np.asarray(final_costs, dtype=np.float64)
+        best_total = totals.min()
+        if not math.isfinite(best_total):
+            raise UsageError("final_costs leave no finite-cost terminus")
+        terminus = totals - best_total
+    fo = np.zeros(t + 2, dtype=np.int64)
+    fo[1:] = np.cumsum([lat.frames[f].n for f in range(t + 1)])
+    fwd = np.ascontiguousarray(np.concatenate([lat.frames[f].costs for f in range(t + 1)]), dtype=np.float64)
+    blks = [lat.block_arrays(b) for b in range(t + 1)]
+    bo = np.zeros(t + 2, dtype=np.int64)
+    bo[1:] = np.cumsum([len(b["arc_id"]) for b in blks])
+
+    def cat(key, dt):
+        return np.ascontiguousarray(np.concatenate([b[key] for b in blks]) if blks else np.empty(0), dtype=dt)
+    frm, to = cat("from_idx", np.int32), cat("to_idx", np.int32)
+    emit = np.ascontiguousarray(cat("ilabel", np.int64) > 0, dtype=np.uint8)
+    g, ac = cat("graph_cost", np.float64), cat("acoustic_cost", np.float64)
+    status = np.ascontiguousarray(np.where(cat("status", np.uint8) == STATUS_LIVE, 0, 1), dtype=np.uint8)
+    extra = cat("extra", np.float64)
+    node_extra = np.zeros(int(fo[-1]))
+    terminus = np.ascontiguousarray(terminus, dtype=np.float64)
+    P64, P32, PD, U8 = _lib.P64, _lib.P32, _lib.PD, C.POINTER(C.c_uint8)
+    L = _lib.lib()
+    rc = L.lb_prune_lattice(int(device), int(t), fo.ctypes.data_as(P64), fwd.ctypes.data_as(PD),
+                            bo.ctypes.data_as(P64), frm.ctypes.data_as(P32), to.ctypes.data_as(P32),
+                            emit.ctypes.data_as(U8), g.ctypes.data_as(PD), ac.ctypes.data_as(PD),
+                            terminus.ctypes.data_as(PD), float(lattice_beam), status.ctypes.data_as(U8),
+                            extra.ctypes.data_as(PD), node_extra.ctypes.data_as(PD))
+    if rc == 4:
+        raise InternalInvariantError(_lib.last_error())
+    if rc != 0:
+        raise UsageError(_lib.last_error())
+    for b in range(t + 1):
+        s_, e_ = int(bo[b]), int(bo[b + 1])
+        lat._blocks[b]["extra"] = extra[s_:e_].copy()
+        lat._blocks[b]["status"] = np.where(status[s_:e_] == 0, STATUS_LIVE, STATUS_PRUNED).astype(np.uint8)
+    ne = list(lat.node_extra) if lat.node_extra is not None else [None] * len(lat.frames)
+    for f in range(t + 1):
+        ne[f] = node_extra[int(fo[f]):int(fo[f + 1])].copy()
+    lat.node_extra = ne
+
+
 def finalize_lattice(lat: WorkLattice) -> FinalLattice:
     """Compact surviving arcs, renumber nodes densely by (frame, idx), sort arcs
     canonically by (from, to, ilabel, olabel, graph, acoustic) — lattice.py:537-598."""

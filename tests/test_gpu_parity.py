@@ -519,3 +519,69 @@ def test_multi_device_replicas_on_one_gpu(oracle_mod):
                                                        devices=(0, 0)))
     single = lb.decode_batch(w, mats[:6], lb.DecodeConfig(beam=12.0, lattice_beam=4.0, max_active=600))
     assert all(a.lattice.same_lattice(b.lattice) for a, b in zip(lat, single))
+
+
+def _work_arrays(lat):
+    from paper_1804_03243_b200.lattice import STATUS_LIVE
+    frames = [f.costs.copy() for f in lat.frames]
+    blocks = []
+    for b in range(len(lat.frames)):
+        a = lat.block_arrays(b)
+        blocks.append({"from_idx": a["from_idx"].astype(np.int64), "to_idx": a["to_idx"].astype(np.int64),
+                       "ilabel": a["ilabel"], "graph_cost": a["graph_cost"].copy(),
+                       "acoustic_cost": a["acoustic_cost"].copy(),
+                       "status": np.where(a["status"] == STATUS_LIVE, 0, 1).astype(np.uint8),
+                       "extra": a["extra"].copy()})
+    return frames, blocks
+
+
+def test_prune_lattice_single_op(oracle_mod):
+    """prune_lattice (lattice.py:365-431) on the device: re-pruning a decoded
+    work lattice with its own beam and final costs is idempotent (the reference's
+    test_reprune_is_idempotent); a tighter beam, and mid-decode prunes from an
+    earlier frontier with a zero terminus, match the CPU restatement
+    (oracle/prune_oracle.py) arc by arc (status exactly, extras within 1e-9)."""
+    from oracle import prune_oracle as PO
+    from paper_1804_03243_b200.lattice import STATUS_LIVE
+    rng = np.random.default_rng(5)
+    checked = 0
+    for seed in range(15_000_000, 15_000_025):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=seed % 2 == 1)
+        try:
+            r = lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0, lattice_beam=5.0, keep_work_lattice=True))
+        except lb.LatbeamError:
+            continue
+        lat = r.work_lattice
+        before = lat.live_arc_table(include_pruned=True)
+        lb.prune_lattice(lat, lat.frames[-1], 5.0, final_costs=lat.final_token_costs)
+        after = lat.live_arc_table(include_pruned=True)
+        assert np.array_equal(before["status"], after["status"])
+        assert np.allclose(before["extra"], after["extra"], equal_nan=True)
+        for _ in range(2):
+            t = int(rng.integers(0, len(lat.frames)))
+            beam = float(rng.uniform(0.0, 5.0))
+            fc = lat.final_token_costs if t == len(lat.frames) - 1 and not r.partial else None
+            frames, blocks = _work_arrays(lat)
+            if fc is None:
+                term = np.zeros(len(frames[t]))
+            else:
+                tot = frames[t] + fc
+                term = tot - tot.min()
+            want, want_ne = PO.prune(frames, blocks, t, beam, term)
+            lb.prune_lattice(lat, lat.frames[t], beam, final_costs=fc)
+            for b in range(t + 1):
+                got = lat.block_arrays(b)
+                st = np.where(got["status"] == STATUS_LIVE, 0, 1)
+                assert np.array_equal(st, want[b]["status"]), (seed, t, b)
+                fin = np.isfinite(want[b]["extra"])
+                assert np.array_equal(np.isfinite(got["extra"]), fin)
+                assert np.allclose(got["extra"][fin], want[b]["extra"][fin], rtol=0, atol=1e-9)
+                assert np.allclose(lat.node_extra[b], want_ne[b], rtol=0, atol=1e-9, equal_nan=True) or \
+                    np.array_equal(np.isinf(lat.node_extra[b]), np.isinf(want_ne[b]))
+            checked += 1
+    assert checked >= 20
+    with pytest.raises(lb.UsageError):
+        lb.prune_lattice(lat, lat.frames[0], -1.0)
+    with pytest.raises(lb.UsageError):
+        lb.prune_lattice(lat, type(lat.frames[0])(0, lat.frames[0].states, lat.frames[0].costs,
+                                                  lat.frames[0].pred_arc, lat.frames[0].pred_idx), 1.0)
