@@ -79,6 +79,14 @@ int lb_decode_batch_device(const lb_graph *g, int32_t n_utts, const double *cons
                            const int32_t *num_frames, int32_t num_labels, const lb_config *cfg,
                            void *stream, lb_result **out);
 
+/* Same, with f32 device-resident cost matrices (what an acoustic model emits;
+ * PAPER.md:376, 483).  Every value is widened exactly to f64 when its row is
+ * loaded (refilling 1-best lanes) or into an HBM scratch first (other modes),
+ * so the result equals decoding the widened f64 matrix. */
+int lb_decode_batch_device_f32(const lb_graph *g, int32_t n_utts, const float *const *dev_costs,
+                               const int32_t *num_frames, int32_t num_labels, const lb_config *cfg,
+                               void *stream, lb_result **out);
+
 /* decode_batch across devices: graphs[k] is a replica of the
  * same graph on some device (lb_graph_create per device; the same device may
  * hold several replicas).  Utterances are split longest-first (lb_shard_lpt),

@@ -32,6 +32,8 @@ SIGNATURES = {
     "lb_decode_batch": (C.c_int, [PV, C.c_int32, C.POINTER(PD), P32, C.c_int32, PV, C.POINTER(PV)]),
     "lb_decode_batch_device": (C.c_int, [PV, C.c_int32, C.POINTER(PD), P32, C.c_int32, PV, PV,
                                          C.POINTER(PV)]),
+    "lb_decode_batch_device_f32": (C.c_int, [PV, C.c_int32, C.POINTER(C.POINTER(C.c_float)), P32, C.c_int32, PV,
+                                             PV, C.POINTER(PV)]),
     "lb_decode_batch_multi": (C.c_int, [C.POINTER(PV), C.c_int32, C.c_int32, C.POINTER(PD), P32, C.c_int32,
                                         PV, C.POINTER(PV)]),
     "lb_shard_lpt": (C.c_int, [C.c_int32, P32, C.c_int32, P32]),

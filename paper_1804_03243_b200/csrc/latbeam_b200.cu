@@ -897,7 +897,7 @@ std::vector<int32_t> lpt_order(int n, const int32_t *T) {
 
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr,
-                const RingDev *ring = nullptr) {
+                const RingDev *ring = nullptr, bool costs_f32 = false) {
     const bool lat = cfg->want_lattice != 0;
     if (lat) {
         // size the arena for what the last lattice decode took, so a steady
@@ -985,6 +985,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     p.exp = ex ? atoi(ex) : 0;
     p.ready = d_ready;
     if (batched && d_ready) return set_err(LB_INTERNAL, "progressive staging needs the lane kernel");
+    p.costs_f32 = costs_f32;
     if (ring) {
         p.ring_ready = ring->ready;
         p.ring_done = ring->done;
@@ -1039,6 +1040,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     // run in waves of `lanes` utterances (the wave's lane l decodes job l).
     const bool refill = !batched && !lat && !packs && d_ready == nullptr && !getenv("LB_NO_REFILL");
     if (ring && !(refill && p.acrow_smem)) return set_err(LB_INTERNAL, "streamed staging needs refilling lanes");
+    if (costs_f32 && !(refill && p.acrow_smem)) return set_err(LB_INTERNAL, "f32 rows need refilling lanes");
     std::vector<UttJob> jq(n);
     if (refill) {
         const std::vector<int32_t> ord = lpt_order(n, T);
@@ -1755,6 +1757,66 @@ int lb_decode_batch_device(const lb_graph *gc, int32_t n, const double *const *d
     std::unique_ptr<lb_result> res(new lb_result());
     cudaStream_t st = stream ? (cudaStream_t)stream : g->stream;
     rc = decode_impl(g, n, dev_costs, T, D, cfg, st, res.get(), 0.0f);
+    if (rc) return rc;
+    *out = res.release();
+    return LB_OK;
+}
+
+int lb_decode_batch_device_f32(const lb_graph *gc, int32_t n, const float *const *dev_costs, const int32_t *T,
+                               int32_t D, const lb_config *cfg, void *stream, lb_result **out) {
+    lb_graph *g = const_cast<lb_graph *>(gc);
+    if (!g || !out) return set_err(LB_USAGE, "graph/out is NULL");
+    *out = nullptr;
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (n < 0 || D < 1) return set_err(LB_USAGE, "bad batch dimensions");
+    if (g->max_ilabel > D) return set_err(LB_USAGE, "graph uses an input label beyond the cost matrix columns");
+    for (int i = 0; i < n; i++)
+        if (T[i] < 1) return set_err(LB_USAGE, "every cost matrix needs T >= 1");
+    std::lock_guard<std::mutex> lock(g->mu);
+    CK(cudaSetDevice(g->device));
+    std::unique_ptr<lb_result> res(new lb_result());
+    cudaStream_t st = stream ? (cudaStream_t)stream : g->stream;
+    bool batched = true;
+    int C = 1;
+    choose_mode(g, n, D, cfg, batched, C);
+    // Refilling 1-best lanes widen each row as they load it into shared memory;
+    // every other mode reads f64 rows, so the batch is widened into HBM first.
+    // Widening f32 -> f64 is exact: the result is the decode of the widened matrix.
+    const bool fused = !batched && !cfg->want_lattice && !cfg->collect_frame_packs &&
+                       (size_t)D * 8 <= ACROW_SMEM_MAX && !getenv("LB_NO_REFILL") && !getenv("LB_F32_WIDEN");
+    if (fused) {
+        rc = decode_impl(g, n, reinterpret_cast<const double *const *>(dev_costs), T, D, cfg, st, res.get(), 0.0f,
+                         nullptr, nullptr, true);
+    } else {
+        std::vector<size_t> off(n + 1, 0);
+        for (int i = 0; i < n; i++) off[i + 1] = off[i] + (((size_t)T[i] * D + 15) & ~(size_t)15);
+        const size_t total = off[n];
+        if (total > g->d_costs_cap) {
+            cudaFree(g->d_costs);
+            g->d_costs = nullptr;
+            g->d_costs_cap = 0;
+            CK(dalloc(&g->d_costs, total));
+            g->d_costs_cap = total;
+        }
+        std::vector<WidenJob> wj(n);
+        std::vector<const double *> dptr(n);
+        for (int i = 0; i < n; i++) {
+            wj[i].src = dev_costs[i];
+            wj[i].dst = g->d_costs + off[i];
+            wj[i].n = (long long)T[i] * D;
+            dptr[i] = g->d_costs + off[i];
+        }
+        WidenJob *d_wj = nullptr;
+        CK(dalloc(&d_wj, (size_t)std::max(n, 1)));
+        struct F { WidenJob *p; ~F() { cudaFree(p); } } fw{d_wj};
+        CK(cudaMemcpyAsync(d_wj, wj.data(), sizeof(WidenJob) * (size_t)n, cudaMemcpyHostToDevice, st));
+        if (n > 0) {
+            widen_f32_kernel<<<dim3(64, (unsigned)n), 256, 0, st>>>(d_wj);
+            CK(cudaGetLastError());
+        }
+        rc = decode_impl(g, n, dptr.data(), T, D, cfg, st, res.get(), 0.0f);
+    }
     if (rc) return rc;
     *out = res.release();
     return LB_OK;

@@ -341,7 +341,11 @@ struct Lane {
 
     __device__ void load_row(const double *r, int frame) {
         row = r;
-        if (p.ready || p.ring_ready) {
+        if (p.costs_f32) {   // f32 log-likelihoods (an acoustic model's output): widened exactly
+            const float *rf = reinterpret_cast<const float *>(r);
+            for (int d = threadIdx.x; d < p.D; d += blockDim.x)
+                lane_dyn[d] = __dmul_rn((double)__ldg(rf + d), p.scale);
+        } else if (p.ready || p.ring_ready) {
             if (p.ready) wait_rows(frame + 1);
             // L2-only loads (ld.cg): a published row was never cached before it was
             // written (the host aligns chunks to 128-byte lines); ld.cv would be
@@ -1090,7 +1094,10 @@ __device__ __forceinline__ void decode_one(const GraphDev &g, const Params &p, c
         if (G.leader()) sm.c_tok += np;
         ln.par = t & 1;
         reset_done = false;
-        ln.load_row(io.costs + (long long)(t - 1) * p.D, t - 1);
+        ln.load_row(p.costs_f32 ? reinterpret_cast<const double *>(reinterpret_cast<const float *>(io.costs) +
+                                                                   (long long)(t - 1) * p.D)
+                                : io.costs + (long long)(t - 1) * p.D,
+                    t - 1);
         if (g.has_eps) ln.fix_preds((t - 1) & 1, t - 1, tbp, np);
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff, t);
@@ -1624,6 +1631,18 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         if (sm.err && !io.out_i[0]) io.out_i[0] = sm.err;
         __stcg(L.round_ctr, sm.round_id);
     }
+}
+
+// f32 -> f64 widening of device-resident cost matrices (exact), one matrix per grid row.
+struct WidenJob {
+    const float *src;
+    double *dst;
+    long long n;
+};
+__global__ void widen_f32_kernel(const WidenJob *__restrict__ jobs) {
+    const WidenJob J = jobs[blockIdx.y];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < J.n; i += (long long)gridDim.x * blockDim.x)
+        J.dst[i] = (double)__ldg(J.src + i);
 }
 
 // Workspace initialisation: every state record idle (pack SENT, no token, minsnap +inf).

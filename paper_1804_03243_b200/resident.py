@@ -20,25 +20,34 @@ from .decoder import DecodeConfig, _raise_status, device_graph, result_timing
 
 def decode_batch_resident(wfst, tensors, config: DecodeConfig | None = None, stream=None,
                           want_lattice: bool = False):
-    """Decode CUDA f64 tensors [T_u, D]; returns (list of dicts, timing dict)."""
+    """Decode CUDA f64 (or f32) tensors [T_u, D]; returns (list of dicts, timing dict)."""
     cfg = config if config is not None else DecodeConfig()
     cfg.validate()
     n = len(tensors)
     if n == 0:
         return [], {}
     D = int(tensors[0].shape[1])
+    dt = str(tensors[0].dtype)
     for t in tensors:
-        if not t.is_cuda or str(t.dtype) != "torch.float64" or not t.is_contiguous() \
-                or t.dim() != 2 or int(t.shape[1]) != D:
-            raise DeviceError("resident decode needs contiguous CUDA float64 [T, D] tensors")
+        if not t.is_cuda or str(t.dtype) != dt or dt not in ("torch.float64", "torch.float32") \
+                or not t.is_contiguous() or t.dim() != 2 or int(t.shape[1]) != D:
+            raise DeviceError("resident decode needs contiguous CUDA float64 or float32 [T, D] tensors "
+                              "of one dtype")
     g = device_graph(wfst, cfg.device)
     L = _lib.lib()
-    cptrs = (PD * n)(*[C.cast(C.c_void_p(t.data_ptr()), PD) for t in tensors])
     T = np.asarray([int(t.shape[0]) for t in tensors], dtype=np.int32)
     c = cfg.to_c(want_lattice, False)
     res = PV()
     sp = C.c_void_p(stream.cuda_stream) if stream is not None else None
-    rc = L.lb_decode_batch_device(g.handle, n, cptrs, ptr(T, P32), D, C.byref(c), sp, C.byref(res))
+    if dt == "torch.float32":
+        # f32 log-likelihoods (an acoustic model's output), widened exactly on the
+        # device: results equal decoding the f64-widened matrices
+        PF = C.POINTER(C.c_float)
+        fptrs = (PF * n)(*[C.cast(C.c_void_p(t.data_ptr()), PF) for t in tensors])
+        rc = L.lb_decode_batch_device_f32(g.handle, n, fptrs, ptr(T, P32), D, C.byref(c), sp, C.byref(res))
+    else:
+        cptrs = (PD * n)(*[C.cast(C.c_void_p(t.data_ptr()), PD) for t in tensors])
+        rc = L.lb_decode_batch_device(g.handle, n, cptrs, ptr(T, P32), D, C.byref(c), sp, C.byref(res))
     _raise_status(rc, _lib.last_error())
     try:
         out = []

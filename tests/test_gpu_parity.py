@@ -585,3 +585,26 @@ def test_prune_lattice_single_op(oracle_mod):
     with pytest.raises(lb.UsageError):
         lb.prune_lattice(lat, type(lat.frames[0])(0, lat.frames[0].states, lat.frames[0].costs,
                                                   lat.frames[0].pred_arc, lat.frames[0].pred_idx), 1.0)
+
+
+@pytest.mark.parametrize("widen", [False, True])
+def test_f32_device_costs_equal_widened_decode(oracle_mod, monkeypatch, widen):
+    """f32 HBM-resident log-likelihoods decode exactly like the f64-widened
+    matrices: fused widening at the row load (refilling lanes) and the HBM
+    widening pass (LB_F32_WIDEN, every other mode), both vs the oracle."""
+    import torch
+
+    from paper_1804_03243_b200.resident import decode_batch_resident
+    if widen:
+        monkeypatch.setenv("LB_F32_WIDEN", "1")
+    w = synthetic.hclg_graph(12, num_states=60_000, pool_size=1500, num_pdfs=300)
+    m32 = [np.ascontiguousarray(m.astype(np.float32)) for m in _ragged_batch(40, 7400)]
+    wide = [m.astype(np.float64) for m in m32]
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=6)
+    outs, _ = decode_batch_resident(w, [torch.from_numpy(m).cuda() for m in m32], cfg)
+    tc, st, _ = oracle_mod.decode_batch_mt(w, wide, 12.0, max_active=600)
+    assert all(st == 0) and [o["total_cost"] for o in outs] == tc.tolist()
+    host = lb.decode_batch(w, wide, cfg, want_lattice=False)
+    for o, r in zip(outs, host):
+        il = w.arc_ilabel[o["path"]]
+        assert r.alignment == list(zip(il[il > 0].tolist(), range(int((il > 0).sum()))))
