@@ -26,8 +26,8 @@ from ._lib import P32, P64, PD, PU64, PV, LbConfig, ptr
 from .acoustics import CostMatrix
 from .errors import (CapacityError, DecodeFailure, DeviceError, InternalInvariantError,
                      UsageError)
-from .lattice import (STATUS_LIVE, STATUS_PRUNED, FinalLattice, FrameTokens, WorkLattice,
-                      finalize_lattice)
+from .lattice import (STATUS_LIVE, STATUS_PRUNED, FinalLattice, FrameTokens, LazyWorkLattice,
+                      WorkLattice, finalize_lattice)
 
 _SCHEDULERS = ("static", "dynamic")
 
@@ -48,8 +48,9 @@ class DecodeConfig:
     cluster size of a lane, 0 = auto), `device` (CUDA ordinal), `devices`
     (several ordinals: `decode_batch` shards the utterances over one graph replica
     per entry, longest first, and returns them in input order),
-    `keep_work_lattice` (also return `DecodeResult.work_lattice`, every live
-    arc with its extra cost; the final lattice is always built on the device).
+    `keep_work_lattice` (ship `DecodeResult.work_lattice`, every live arc with
+    its extra cost, with the result; otherwise a lattice decode returns a
+    `LazyWorkLattice` that re-decodes on first use -- same lattice, bit-exact).
     """
 
     beam: float = 14.0
@@ -346,6 +347,8 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
                          None, counters)
         if want_lattice:
             r.lattice = _final_lattice(res, u, m.shape[0])
+            if not cfg.keep_work_lattice:
+                r.work_lattice = LazyWorkLattice(_work_thunk(wfst, m, cfg))
         if collect_frame_packs or (want_lattice and cfg.keep_work_lattice):
             try:
                 _attach_lattice(r, wfst, res, u, m, cfg, ntok.value, nlat.value,
@@ -360,6 +363,17 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
                          "launches": tm["launches"], "total": time.perf_counter() - t0}
         out.append(r)
     return out
+
+
+def _work_thunk(wfst, m, cfg):
+    """Re-decode one utterance keeping its work lattice (LazyWorkLattice)."""
+    from dataclasses import replace
+
+    def build():
+        c = replace(cfg, keep_work_lattice=True, devices=(), lanes=0,
+                    device=int(cfg.devices[0]) if cfg.devices else cfg.device)
+        return decode_utterance(wfst, m, c, want_lattice=True).work_lattice
+    return build
 
 
 def _final_lattice(res, u, num_frames) -> FinalLattice:

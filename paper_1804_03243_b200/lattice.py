@@ -166,6 +166,33 @@ class WorkLattice:
                 for i in range(len(t["slots"]))]
 
 
+class LazyWorkLattice(WorkLattice):
+    """A WorkLattice built on first use.
+
+    The reference returns `DecodeResult.work_lattice` whenever a lattice is
+    requested (decoder.py:605-606).  Shipping every live arc and token list to
+    the host costs more than the decode itself (C1: ~12.6M arcs per utterance),
+    so results carry this proxy instead: the first attribute access re-decodes
+    the utterance with `keep_work_lattice=True` -- decoding is deterministic and
+    bit-exact, so it is the same lattice -- and adopts it."""
+
+    def __init__(self, build):   # noqa: D401 - no WorkLattice state until built
+        self.__dict__["_build"] = build
+
+    def _materialise(self):
+        build = self.__dict__.get("_build")
+        if build is not None:
+            real = build()
+            self.__dict__["_build"] = None
+            self.__dict__.update(real.__dict__)
+
+    def __getattr__(self, name):
+        if name.startswith("__") or self.__dict__.get("_build") is None:
+            raise AttributeError(name)
+        self._materialise()
+        return getattr(self, name)
+
+
 def prune_lattice(lat: WorkLattice, frontier: FrameTokens, lattice_beam: float,
                   final_costs: np.ndarray | None = None, device: int = 0) -> None:
     """Flag arcs whose extra cost exceeds lattice_beam (lattice.py:365-431 of

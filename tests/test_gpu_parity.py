@@ -608,3 +608,20 @@ def test_f32_device_costs_equal_widened_decode(oracle_mod, monkeypatch, widen):
     for o, r in zip(outs, host):
         il = w.arc_ilabel[o["path"]]
         assert r.alignment == list(zip(il[il > 0].tolist(), range(int((il > 0).sum()))))
+
+
+def test_work_lattice_by_default():
+    """DecodeResult.work_lattice exists whenever a lattice is requested
+    (decoder.py:605-606): a LazyWorkLattice that materialises on first use and
+    equals the eagerly kept one; 1-best decodes have none."""
+    from paper_1804_03243_b200.lattice import WorkLattice
+    w, m = synthetic.random_task(21, allow_eps_cycles=True)
+    lazy = lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0, lattice_beam=4.0))
+    eager = lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0, lattice_beam=4.0, keep_work_lattice=True))
+    assert isinstance(lazy.work_lattice, WorkLattice)
+    a = lazy.work_lattice.live_arc_table(include_pruned=True)
+    b = eager.work_lattice.live_arc_table(include_pruned=True)
+    assert set(a) == set(b) and all(np.array_equal(a[k], b[k]) for k in a)
+    assert lazy.work_lattice.num_frames == eager.work_lattice.num_frames
+    assert [f.states.tolist() for f in lazy.work_lattice.frames] == [f.states.tolist() for f in eager.work_lattice.frames]
+    assert lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0), want_lattice=False).work_lattice is None
