@@ -135,6 +135,8 @@ struct Workspace {
     unsigned long long *tok_pack = nullptr, *ne_enc = nullptr;
     long long *tok_base = nullptr, *lat_base = nullptr, *out_c = nullptr;
     LaneWs *d_lanes = nullptr;
+    LaneWs *d_lanes_mix = nullptr;   // the same lanes with per-lane cluster widths (mixed-width launches)
+    std::vector<LaneWs> h_lanes;
     UttDesc *d_desc = nullptr;
     LaneCtl *d_ctl = nullptr;   // batched mode: per-lane control blocks
     std::vector<void *> owned;
@@ -184,6 +186,8 @@ struct lb_graph {
     double *fin = nullptr;
     int64_t bytes = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;              // second launch stream (mixed-width lanes)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex mu;
     Workspace ws;    // decode lanes
     Workspace ws1;   // the single-op surfaces (expand_*): one small lane, never evicts ws
@@ -279,6 +283,7 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     CK(A(&w.tok_base, (size_t)(tmax + 2) * nl));
     CK(A(&w.lat_base, (size_t)(tmax + 2) * nl));
     CK(A(&w.d_lanes, nl));
+    CK(A(&w.d_lanes_mix, nl));
     CK(A(&w.d_desc, nl));
     CK(A(&w.d_ctl, nl));
     init_rec<<<g->sms * 4, 256, 0, g->stream>>>(w.rec, (long long)(S * nl));
@@ -303,6 +308,7 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
         x.C = C;
     }
     CK(cudaMemcpyAsync(w.d_lanes, hl.data(), nl * sizeof(LaneWs), cudaMemcpyHostToDevice, g->stream));
+    w.h_lanes = hl;
     CK(cudaStreamSynchronize(g->stream));
     w.lanes = lanes;
     w.C = C;
@@ -945,11 +951,23 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
                                        (int64_t)(bpl * BNW + 1) * BCCH
                                  : cand_capacity(g, max_tok, C, threads);
     // lanes: requested, else as many as fit a memory budget (<= 1 wave of SMs)
-    const size_t per_lane = lane_bytes(S, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+
     int lanes = batched ? lanes_guess : (cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / C)));
     lanes = std::max(1, std::min(lanes, n > 0 ? n : 1));
+    // Refilling 1-best lanes (see below).  When the requested lanes leave SMs
+    // idle (64 two-CTA lanes use 128 of 148), the first `n3` lanes run as
+    // three-CTA clusters in a concurrent launch on the same job queue, so every
+    // SM decodes (still `lanes` lanes; a wider lane just takes more jobs).
+    const bool refill_mode = !batched && !lat && !packs && d_ready == nullptr && !getenv("LB_NO_REFILL");
+    int n3 = 0;
+    if (refill_mode && C == 2 && cfg->ctas_per_lane == 0 && n > lanes && !getenv("LB_NO_MIXED"))
+        n3 = std::max(0, std::min(lanes, g->sms - 2 * lanes));
+    if (const char *e = getenv("LB_MIXED_N3")) n3 = std::max(0, std::min(lanes, atoi(e)));
+    const int Ca = n3 > 0 ? 3 : C;   // CTA segments allocated per lane
+    if (getenv("LB_MODE_DEBUG")) fprintf(stderr, "[lanes] %d lanes, %d of them 3-CTA, C=%d\n", lanes, n3, C);
+    const size_t per_lane = lane_bytes(S, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
     const Workspace &w0 = g->ws;
-    const bool fits = w0.lanes >= lanes && w0.C == C && w0.S == g->S && w0.ccap >= ccap && w0.tok_cap >= tok_cap &&
+    const bool fits = w0.lanes >= lanes && w0.C == Ca && w0.S == g->S && w0.ccap >= ccap && w0.tok_cap >= tok_cap &&
                       w0.lat_cap >= lat_cap && w0.path_cap >= path_cap && w0.tmax >= tmax && (w0.packs || !packs) &&
                       (w0.lat || !lat);
     if (!fits) {   // size the lane count to the device memory left (the workspace is reused across calls)
@@ -964,7 +982,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         if ((size_t)lanes * per_lane > budget)
             return set_err(LB_CAPACITY, "not enough device memory for one decode lane; lower token_arena / max_lattice_arcs");
     }
-    int rc = ensure_workspace(g, g->ws, lanes, C, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    int rc = ensure_workspace(g, g->ws, lanes, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
     if (rc) return rc;
     Workspace &w = g->ws;
 
@@ -1038,7 +1056,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     // ragged batch never waits for a wave's longest utterance.  Lattice and
     // token-list decodes keep their per-utterance arenas until readback, so they
     // run in waves of `lanes` utterances (the wave's lane l decodes job l).
-    const bool refill = !batched && !lat && !packs && d_ready == nullptr && !getenv("LB_NO_REFILL");
+    const bool refill = refill_mode;
     if (ring && !(refill && p.acrow_smem)) return set_err(LB_INTERNAL, "streamed staging needs refilling lanes");
     if (costs_f32 && !(refill && p.acrow_smem)) return set_err(LB_INTERNAL, "f32 rows need refilling lanes");
     std::vector<UttJob> jq(n);
@@ -1099,9 +1117,38 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc,
-                                  (const UttJob *)(w.d_jobs + (refill ? 0 : w0)), nj, refill ? w.queue : nullptr));
-            res->launches++;
+            if (n3 > 0) {
+                // lanes [0, n3) as 3-CTA clusters on a forked stream, the rest as
+                // 2-CTA clusters here; both claim from the same queue
+                std::vector<LaneWs> hm(w.h_lanes.begin(), w.h_lanes.begin() + nw);
+                for (int l = 0; l < nw; l++) hm[l].C = l < n3 ? 3 : 2;
+                CK(cudaMemcpyAsync(w.d_lanes_mix, hm.data(), nw * sizeof(LaneWs), cudaMemcpyHostToDevice, st));
+                if (!g->stream2) CK(cudaStreamCreateWithFlags(&g->stream2, cudaStreamNonBlocking));
+                if (!g->ev_fork) CK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+                if (!g->ev_join) CK(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+                CK(cudaEventRecord(g->ev_fork, st));
+                CK(cudaStreamWaitEvent(g->stream2, g->ev_fork, 0));
+                cudaLaunchConfig_t l3 = lc;
+                cudaLaunchAttribute a3[1];
+                a3[0] = at[0];
+                a3[0].val.clusterDim.x = 3;
+                l3.attrs = a3;
+                l3.gridDim = dim3((unsigned)(n3 * 3));
+                l3.stream = g->stream2;
+                CK(cudaLaunchKernelEx(&l3, kern, gd, p, (const LaneWs *)w.d_lanes_mix, (const UttDesc *)w.d_desc,
+                                      (const UttJob *)w.d_jobs, nj, w.queue));
+                lc.gridDim = dim3((unsigned)((nw - n3) * 2));
+                if (nw > n3)
+                    CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)(w.d_lanes_mix + n3),
+                                          (const UttDesc *)(w.d_desc + n3), (const UttJob *)w.d_jobs, nj, w.queue));
+                CK(cudaEventRecord(g->ev_join, g->stream2));
+                CK(cudaStreamWaitEvent(st, g->ev_join, 0));
+                res->launches += nw > n3 ? 2 : 1;
+            } else {
+                CK(cudaLaunchKernelEx(&lc, kern, gd, p, (const LaneWs *)w.d_lanes, (const UttDesc *)w.d_desc,
+                                      (const UttJob *)(w.d_jobs + (refill ? 0 : w0)), nj, refill ? w.queue : nullptr));
+                res->launches++;
+            }
         }
         CK(cudaEventRecord(e1, st));
         if (lat) {
@@ -1482,6 +1529,9 @@ int lb_graph_destroy(lb_graph *g) {
     if (g->ring) cudaFreeHost(g->ring);
     if (g->ring_ctl) cudaFreeHost(g->ring_ctl);
     if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->stream2) cudaStreamDestroy(g->stream2);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_join) cudaEventDestroy(g->ev_join);
     delete g;
     return LB_OK;
 }
