@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -123,7 +124,13 @@ struct Workspace {
     int path_cap = 0, tmax = 0;
     bool packs = false, lat = false;
     // lane scratch
+    bool batched = false;      // batched-mode layout (StateRec) vs persistent-lane layout
     StateRec *rec = nullptr;
+    unsigned long long *pk = nullptr;
+    int *tokidx = nullptr, *tpred = nullptr;
+    ERec *erec = nullptr;
+    double *msnap = nullptr, *tcost = nullptr, *f0cost = nullptr;
+    unsigned *tarc = nullptr, *etouched = nullptr;
     EpsWin *rpk = nullptr;
     unsigned *tag = nullptr, *touched = nullptr, *fr = nullptr, *fix = nullptr, *round_ctr = nullptr;
     int4 *cand = nullptr;
@@ -163,9 +170,12 @@ struct Workspace {
 
 // Device bytes of one lane's scratch + slot (the lane-count budget).
 size_t lane_bytes(int64_t S, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap, int path_cap, int tmax,
-                  bool packs, bool lat) {
-    (void)lat;
-    return (size_t)S * (32 + 32 + 4 + (size_t)C * 16) + (size_t)C * ccap * 20 +
+                  bool packs, bool lat, bool batched) {
+    // per state: rpk 32 + tag 4 + fr/fix (12 per CTA), then the mode's own layout
+    const size_t per_state = batched ? 32 + 32 + 4 + (size_t)C * 16
+                                     : 8 + 4 + 16 + 8 + 32 + 4 + (size_t)C * 16;   // pk tokidx erec msnap rpk tag
+    const size_t per_cand = batched ? 20 + 4 : 20 + 4 + 8 + 4 + 4 + 8 + 4;       // + winner payload, f0cost
+    return (size_t)S * per_state + (size_t)C * ccap * per_cand +
            (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) + (size_t)lat_cap * 28 + (size_t)path_cap * 4 +
            (size_t)(tmax + 2) * 16 + 256;
 }
@@ -242,9 +252,10 @@ struct lb_result {
 namespace {
 
 int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, int64_t tok_cap, int64_t lat_cap,
-                     int path_cap, int tmax, bool packs, bool lat) {
+                     int path_cap, int tmax, bool packs, bool lat, bool batched) {
     if (w.lanes >= lanes && w.C == C && w.S == g->S && w.ccap >= ccap && w.tok_cap >= tok_cap &&
-        w.lat_cap >= lat_cap && w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat))
+        w.lat_cap >= lat_cap && w.path_cap >= path_cap && w.tmax >= tmax && (w.packs || !packs) && (w.lat || !lat) &&
+        w.batched == batched)
         return LB_OK;
     // Reallocate to exactly this request (never the max of old and new: the
     // lane budget in decode_impl was computed for this request alone).
@@ -256,10 +267,24 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
         if (e == cudaSuccess) w.owned.push_back((void *)*p);
         return e;
     };
-    CK(A(&w.rec, S * nl));
+    const size_t cc = (size_t)ccap;
+    if (batched) {
+        CK(A(&w.rec, S * nl));
+        CK(A(&w.touched, nc * S * nl));
+    } else {
+        CK(A(&w.pk, S * nl));
+        CK(A(&w.tokidx, S * nl));
+        CK(A(&w.erec, S * nl));
+        CK(A(&w.msnap, S * nl));
+        CK(A(&w.touched, nc * cc * nl));
+        CK(A(&w.tcost, nc * cc * nl));
+        CK(A(&w.tpred, nc * cc * nl));
+        CK(A(&w.tarc, nc * cc * nl));
+        CK(A(&w.f0cost, nc * cc * nl));
+        CK(A(&w.etouched, nc * S * nl));
+    }
     CK(A(&w.rpk, 2 * S * nl));
     CK(A(&w.tag, S * nl));
-    CK(A(&w.touched, nc * S * nl));
     CK(A(&w.fr, 2 * nc * S * nl));
     CK(A(&w.fix, nc * S * nl));
     CK(A(&w.cand, nc * (size_t)ccap * nl));
@@ -286,7 +311,13 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     CK(A(&w.d_lanes_mix, nl));
     CK(A(&w.d_desc, nl));
     CK(A(&w.d_ctl, nl));
-    init_rec<<<g->sms * 4, 256, 0, g->stream>>>(w.rec, (long long)(S * nl));
+    if (batched) {
+        init_rec<<<g->sms * 4, 256, 0, g->stream>>>(w.rec, (long long)(S * nl));
+    } else {
+        CK(cudaMemsetAsync(w.pk, 0xFF, S * nl * 8, g->stream));       // SENT
+        CK(cudaMemsetAsync(w.tokidx, 0xFF, S * nl * 4, g->stream));   // -1
+        fill_f64<<<g->sms * 4, 256, 0, g->stream>>>(w.msnap, (long long)(S * nl), std::numeric_limits<double>::infinity());
+    }
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(w.rpk, 0xFF, 2 * S * nl * sizeof(EpsWin), g->stream));
     CK(cudaMemsetAsync(w.tag, 0, S * nl * 4, g->stream));
@@ -294,10 +325,24 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     std::vector<LaneWs> hl(nl);
     for (size_t l = 0; l < nl; l++) {
         LaneWs &x = hl[l];
-        x.rec = w.rec + l * S;
+        std::memset(&x, 0, sizeof(x));
+        if (batched) {
+            x.rec = w.rec + l * S;
+            x.touched = w.touched + l * nc * S;
+        } else {
+            x.pk = w.pk + l * S;
+            x.tokidx = w.tokidx + l * S;
+            x.erec = w.erec + l * S;
+            x.msnap = w.msnap + l * S;
+            x.touched = w.touched + l * nc * cc;
+            x.tcost = w.tcost + l * nc * cc;
+            x.tpred = w.tpred + l * nc * cc;
+            x.tarc = w.tarc + l * nc * cc;
+            x.f0cost = w.f0cost + l * nc * cc;
+            x.etouched = w.etouched + l * nc * S;
+        }
         x.rpk = w.rpk + l * 2 * S;
         x.tag = w.tag + l * S;
-        x.touched = w.touched + l * nc * S;
         x.fr = w.fr + l * 2 * nc * S;
         x.fix = w.fix + l * nc * S;
         x.cand = w.cand + l * nc * (size_t)ccap;
@@ -320,6 +365,7 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     w.tmax = tmax;
     w.packs = packs;
     w.lat = lat;
+    w.batched = batched;
     return LB_OK;
 }
 
@@ -965,9 +1011,9 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     if (const char *e = getenv("LB_MIXED_N3")) n3 = std::max(0, std::min(lanes, atoi(e)));
     const int Ca = n3 > 0 ? 3 : C;   // CTA segments allocated per lane
     if (getenv("LB_MODE_DEBUG")) fprintf(stderr, "[lanes] %d lanes, %d of them 3-CTA, C=%d\n", lanes, n3, C);
-    const size_t per_lane = lane_bytes(S, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    const size_t per_lane = lane_bytes(S, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat, batched);
     const Workspace &w0 = g->ws;
-    const bool fits = w0.lanes >= lanes && w0.C == Ca && w0.S == g->S && w0.ccap >= ccap && w0.tok_cap >= tok_cap &&
+    const bool fits = w0.batched == batched && w0.lanes >= lanes && w0.C == Ca && w0.S == g->S && w0.ccap >= ccap && w0.tok_cap >= tok_cap &&
                       w0.lat_cap >= lat_cap && w0.path_cap >= path_cap && w0.tmax >= tmax && (w0.packs || !packs) &&
                       (w0.lat || !lat);
     if (!fits) {   // size the lane count to the device memory left (the workspace is reused across calls)
@@ -975,14 +1021,15 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         CK(cudaMemGetInfo(&free_b, &total_b));
         // the current workspace is freed before the new one is allocated, whatever its shape
         const size_t reuse = w0.lanes > 0 ? (size_t)w0.lanes * lane_bytes(S, w0.C, w0.ccap, w0.tok_cap, w0.lat_cap,
-                                                                           w0.path_cap, w0.tmax, w0.packs, w0.lat)
+                                                                           w0.path_cap, w0.tmax, w0.packs, w0.lat,
+                                                                           w0.batched)
                                           : 0;
         const size_t budget = (size_t)((double)(free_b + reuse) * 0.85);
         while (lanes > 1 && (size_t)lanes * per_lane > budget) lanes--;
         if ((size_t)lanes * per_lane > budget)
             return set_err(LB_CAPACITY, "not enough device memory for one decode lane; lower token_arena / max_lattice_arcs");
     }
-    int rc = ensure_workspace(g, g->ws, lanes, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat);
+    int rc = ensure_workspace(g, g->ws, lanes, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat, batched);
     if (rc) return rc;
     Workspace &w = g->ws;
 
@@ -2297,8 +2344,9 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     if (!g || !states || !costs || n < 1) return set_err(LB_USAGE, "frontier is empty");
     std::lock_guard<std::mutex> lock(g->mu);
     CK(cudaSetDevice(g->device));
-    const int64_t ccap = std::min<int64_t>(g->A_emit, n * g->max_edeg) + 25 * CAND_CHUNK;
-    int rc = ensure_workspace(g, g->ws1, 1, 1, ccap, n + g->S, 0, 16, 1, false, false);
+    // the frontier itself sits in the winner / round-0 lists (expand_nonemitting)
+    const int64_t ccap = std::max<int64_t>(std::min<int64_t>(g->A_emit, n * g->max_edeg) + 25 * CAND_CHUNK, n);
+    int rc = ensure_workspace(g, g->ws1, 1, 1, ccap, n + g->S, 0, 16, 1, false, false, false);
     if (rc) return rc;
     Workspace &w = g->ws1;
     cudaStream_t st = g->stream;

@@ -204,11 +204,24 @@ struct __align__(16) EpsWin {
 #define CAND_LD __ldcs
 #endif
 
+// Epsilon-improved state: its final f64 cost and predecessor (source state << 1).
+struct __align__(16) ERec {
+    double cost;
+    int pred;
+    int _pad;
+};
+
+// Per-lane scratch.  The batched mode keeps one 32-byte StateRec per state
+// (`rec`); the persistent lanes keep only what the hot phases touch per state
+// -- the 8-byte recombination word `pk` and the 4-byte token index -- and carry
+// every winner's cost / predecessor / arc in compact, coalesced per-frame lists
+// (`touched` + `tcost` / `tpred` / `tarc`), so 64 lanes' hot per-state data fit
+// in L2.  Epsilon-improved states (few) keep theirs in `erec`.
 struct LaneWs {
-    StateRec *rec;             // [S]
+    StateRec *rec;             // [S] batched mode only
     EpsWin *rpk;               // [2][S] epsilon round winners by round parity
     unsigned *tag;             // [S] epsilon round tag
-    unsigned *touched;         // [C][S] states touched this frame
+    unsigned *touched;         // batched: [C][S] states touched; lanes: [C][ccap] emitting winners
     unsigned *fr;              // [2][C][S] epsilon frontier by round parity
     unsigned *fix;             // [C][S] tokens whose predecessor is an epsilon source state
     int4 *cand;                // [C][ccap] emitting candidates {dst|flag, arc, cost_lo, cost_hi}
@@ -217,6 +230,16 @@ struct LaneWs {
     unsigned *round_ctr;       // persistent per-lane round counter
     int S;
     int C;
+    // persistent lanes only
+    unsigned long long *pk;    // [S] recombination word (cost key << 32 | arc), SENT = untouched
+    int *tokidx;               // [S] index of the state's token in the newest frame's list
+    ERec *erec;                // [S] epsilon-improved states' cost / predecessor
+    double *msnap;             // [S] min epsilon-source snapshot (lattice rule A.5), +inf idle
+    double *tcost;             // [C][ccap] winner cost of touched[k]
+    int *tpred;                // [C][ccap] winner predecessor ((token << 1) | 1)
+    unsigned *tarc;            // [C][ccap] winner arc
+    double *f0cost;            // [C][ccap] round-0 epsilon frontier costs (seeds)
+    unsigned *etouched;        // [C][S] states first reached by an epsilon offer this frame
 };
 
 // One utterance slot of a wave.
@@ -372,6 +395,23 @@ __device__ __forceinline__ unsigned atom_exch_u32(unsigned *a, unsigned v) {
     asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(a), "r"(v) : "memory");
 #endif
     return o;
+}
+
+__device__ __forceinline__ unsigned long long atom_exch_u64(unsigned long long *a, unsigned long long v) {
+    unsigned long long o;
+#ifdef LB_L2HINT
+    asm volatile("atom.relaxed.gpu.global.exch.L2::cache_hint.b64 %0, [%1], %2, %3;" : "=l"(o) : "l"(a), "l"(v), "l"(l2_pol()) : "memory");
+#else
+    asm volatile("atom.relaxed.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(a), "l"(v) : "memory");
+#endif
+    return o;
+}
+__device__ __forceinline__ void rst_i32(int *a, int v) {
+#ifdef LB_L2HINT
+    asm volatile("st.global.cg.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_pol()) : "memory");
+#else
+    __stcg(a, v);
+#endif
 }
 
 // Fire-and-forget 64-bit min at L2 (REDG): the issuing thread never waits.

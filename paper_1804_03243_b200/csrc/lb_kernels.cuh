@@ -55,7 +55,7 @@ struct Smem {
     int err, err_frame;
     long long err_aux;
     // per CTA
-    int ntouched[2], ncand[2], nseed[2], nfix[2];
+    int ntouched[2], ncand[2], nseed[2], nfix[2], netouched[2];
     int nfr[3];
     unsigned long long best[2];    // order-preserving f64 running best (frame parity)
     unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
@@ -214,8 +214,9 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, in
 // state, arc, key, pred} and a u32 fix stage.
 constexpr int SWT = 64;
 constexpr size_t ACROW_SMEM_MAX = 48 * 1024;   // acoustic rows up to 6144 pdfs live in shared memory
-constexpr int WSCR = SWT * 32 + SW * 4;
-static_assert(2 * SW * 4 <= WSCR, "winners stages fit the warp scratch");
+constexpr int SWW = 96;   // winners stages: touched {v, arc, pred, cost} and round-0 frontier {v, cost}
+constexpr int WSCR = (SWT * 32 + SW * 4) > SWW * 32 ? (SWT * 32 + SW * 4) : SWW * 32;
+static_assert(SWW * 20 + SWW * 12 <= WSCR, "winners stages fit the warp scratch");
 inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem) {
     const size_t nw = (size_t)threads / 32;
     return (acrow_smem ? (size_t)D * 8 : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
@@ -300,7 +301,10 @@ struct Lane {
     }
 
     // this CTA's segments of the per-CTA lists
-    __device__ __forceinline__ unsigned *touched() const { return L.touched + (size_t)G.rank * L.S; }
+    // emitting winners of this CTA (with their payload) and epsilon-reached states
+    __device__ __forceinline__ size_t cseg() const { return (size_t)G.rank * L.ccap; }
+    __device__ __forceinline__ unsigned *touched() const { return L.touched + cseg(); }
+    __device__ __forceinline__ unsigned *etouched() const { return L.etouched + (size_t)G.rank * L.S; }
     __device__ __forceinline__ unsigned *front(int r) const {
         return L.fr + ((size_t)(r & 1) * L.C + G.rank) * L.S;
     }
@@ -361,7 +365,7 @@ struct Lane {
         const int q = par ^ 1;
         if (G.leader()) G.M->ntok[q] = G.M->nlat[q] = 0;
         if (threadIdx.x == 0) {
-            lane_sm.ntouched[q] = lane_sm.ncand[q] = lane_sm.nseed[q] = lane_sm.nfix[q] = 0;
+            lane_sm.ntouched[q] = lane_sm.ncand[q] = lane_sm.nseed[q] = lane_sm.nfix[q] = lane_sm.netouched[q] = 0;
             lane_sm.best[q] = SENT;
         }
     }
@@ -379,7 +383,7 @@ struct Lane {
     // with sentinels (x = -1) that winners() skips.
     static constexpr int CCH = CAND_CHUNK;
     __device__ double emit(const unsigned *pts, const double *ptc, int np, double beam_eff, int frame) {
-        StateRec *rec = L.rec;
+        unsigned long long *pk = L.pk;
         unsigned c_scan = 0, c_cand = 0;
         int *ncand = &lane_sm.ncand[par];
         int4 *cb = L.cand + (size_t)G.rank * L.ccap;
@@ -435,7 +439,7 @@ struct Lane {
                 if (cand[u] < inf_d()) {
                     const unsigned long long word = pack_word(cand[u], aa[u]);
                     em[u] = (unsigned)(word >> 32) <= bound_key;
-                    if (em[u]) red_min_u64(&rec[r[u].x].pack, word);
+                    if (em[u]) red_min_u64(pk + r[u].x, word);
                 }
                 const unsigned bb = __ballot_sync(FULL, em[u]);
                 off[u] = tot + __popc(bb & lt);
@@ -497,7 +501,7 @@ struct Lane {
         for (int q = threadIdx.x; q < mine; q += blockDim.x) {
             const long long o = tbf + (long long)__ldcg(fx + q);
             const int u = __ldcg(io.tok_pred + o) >> 1;
-            const int pi = rld_i32(&L.rec[u].tokidx);
+            const int pi = rld_i32(L.tokidx + u);
             if (pi < 0 || pi >= nf || __ldcg(io.tok_state + tbf + pi) != (unsigned)u)
                 set_error(E_INT_EPS_PRED, frame, u);
             __stcg(io.tok_pred + o, pi << 1);
@@ -506,10 +510,56 @@ struct Lane {
 
     // ---- winners: owners of the state words; seeds; epsilon frontier (round 0); histogram ----
     // Warp-uniform loop over the CTA's candidate buffer (32*WUNR entries per warp
-    // step).  Appends go through per-warp shared-memory stages; the max-active
-    // histogram is per warp (match_any groups equal bins, the group leader does a
-    // plain read-modify-write) and is summed into the CTA histogram at the end,
-    // so no shared-memory atomic is ever contended.
+    // step).  A candidate owns its state iff the state's final word is its own
+    // word (arc ids make words unique).  The owner's payload {state, arc,
+    // predecessor, f64 cost} goes to this CTA's touched list and, for a seed
+    // with epsilon arcs, {state, cost} to the round-0 frontier -- both through
+    // per-warp shared-memory stages flushed in bulk (one counter atomic per
+    // flush, coalesced writes), so no per-state record is written here.  The
+    // max-active histogram is per warp and summed into the CTA histogram at the
+    // end, so no shared-memory atomic is ever contended.
+    struct WinStage {   // per-warp stage of owner payloads (SWW entries)
+        unsigned *v, *a;
+        int *p;
+        double *c;
+        int n;
+    };
+    struct FrStage {    // per-warp stage of round-0 frontier entries (SWW entries)
+        unsigned *v;
+        double *c;
+        int n;
+    };
+    __device__ __forceinline__ void win_flush(WinStage &st, int *counter) const {
+        __syncwarp();
+        if (st.n == 0) return;
+        int base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, st.n);
+        base = __shfl_sync(FULL, base, 0);
+        const size_t o = cseg() + base;
+        for (int i = threadIdx.x & 31; i < st.n; i += 32) {
+            __stcg(L.touched + o + i, st.v[i]);
+            __stcg(L.tarc + o + i, st.a[i]);
+            __stcg(L.tpred + o + i, st.p[i]);
+            __stcg(L.tcost + o + i, st.c[i]);
+        }
+        __syncwarp();
+        st.n = 0;
+    }
+    __device__ __forceinline__ void fr_flush(FrStage &st, int *counter, unsigned *out) const {
+        __syncwarp();
+        if (st.n == 0) return;
+        int base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, st.n);
+        base = __shfl_sync(FULL, base, 0);
+        double *oc = L.f0cost + cseg() + base;
+        for (int i = threadIdx.x & 31; i < st.n; i += 32) {
+            __stcg(out + base + i, st.v[i]);
+            __stcg(oc + i, st.c[i]);
+        }
+        __syncwarp();
+        st.n = 0;
+    }
+
     __device__ void winners(double cutoff, double best) {
         const int nc = lane_sm.ncand[par];
         const bool hist = p.max_active > 0;
@@ -517,39 +567,28 @@ struct Lane {
         const double inv_w = __drcp_rn(width);
         const int4 *cb = L.cand + (size_t)G.rank * L.ccap;
         const int *cbi = L.candi + (size_t)G.rank * L.ccap;
-        StateRec *rec = L.rec;
-        unsigned *tl = touched();
+        const unsigned long long *pk = L.pk;
         unsigned *f0 = front(0);
         int *ntouched = &lane_sm.ntouched[par], *nf0 = &lane_sm.nfr[0];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        const unsigned lt = (1u << lane) - 1u;
         int *wh = whist_all() + warp * NBINS;
         if (hist)
             for (int b = lane; b < NBINS; b += 32) wh[b] = 0;
         __syncwarp();
-        WStage st_t = stage(0), st_f = stage(1);
+        char *scr = scratch();
+        WinStage sw;
+        sw.c = reinterpret_cast<double *>(scr);
+        sw.v = reinterpret_cast<unsigned *>(sw.c + SWW);
+        sw.a = sw.v + SWW;
+        sw.p = reinterpret_cast<int *>(sw.a + SWW);
+        sw.n = 0;
+        FrStage sf;
+        sf.c = reinterpret_cast<double *>(sw.p + SWW);
+        sf.v = reinterpret_cast<unsigned *>(sf.c + SWW);
+        sf.n = 0;
         unsigned nseed = 0;
         const unsigned long long t0 = wbegin();
-        if (p.exp & 4) {   // timing probe: the loop's loads and owner test only
-            unsigned nown = 0;
-            for (int kb = warp * 32 * WUNR; kb < nc; kb += nw * 32 * WUNR) {
-                int4 e[WUNR];
-#pragma unroll
-                for (int u = 0; u < WUNR; u++) {
-                    const int k = kb + u * 32 + lane;
-                    e[u].x = -1;
-                    if (k < nc) e[u] = __ldcg(cb + k);
-                }
-                unsigned long long pk[WUNR];
-#pragma unroll
-                for (int u = 0; u < WUNR; u++)
-                    pk[u] = e[u].x != -1 ? rld_u64(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
-#pragma unroll
-                for (int u = 0; u < WUNR; u++)
-                    nown += e[u].x != -1 && pk[u] == pack_word(__hiloint2double(e[u].w, e[u].z), (unsigned)e[u].y);
-            }
-            if (nown == 0xFFFFFFFFu) lane_sm.err_aux = nown;
-            if (p.exp & 8) { wend(2, t0); return; }
-        }
         // candidate records of the next batch are fetched one batch ahead
         int4 en[WUNR];
         int tn[WUNR];
@@ -577,26 +616,42 @@ struct Lane {
                     tn[u] = CAND_LD(cbi + k);
                 }
             }
-            unsigned long long pk[WUNR];
+            unsigned long long pw[WUNR];
 #pragma unroll
             for (int u = 0; u < WUNR; u++)
-                pk[u] = e[u].x != -1 ? rld_u64(&rec[(unsigned)e[u].x & ~EPS_FLAG].pack) : 0ull;
+                pw[u] = e[u].x != -1 ? rld_u64(pk + ((unsigned)e[u].x & ~EPS_FLAG)) : 0ull;
 #pragma unroll
             for (int u = 0; u < WUNR; u++) {
                 const unsigned v = (unsigned)e[u].x & ~EPS_FLAG;
                 const double cand = __hiloint2double(e[u].w, e[u].z);
-                const bool own = e[u].x != -1 && pk[u] == pack_word(cand, (unsigned)e[u].y);
-                if (own) store_winner(&rec[v], cand, (ti[u] << 1) | 1);
-                st_t.push(own, v, ntouched, tl);
+                const bool own = e[u].x != -1 && pw[u] == pack_word(cand, (unsigned)e[u].y);
+                const unsigned mo = __ballot_sync(FULL, own);
+                if (own) {
+                    const int j = sw.n + __popc(mo & lt);
+                    sw.v[j] = v;
+                    sw.a[j] = (unsigned)e[u].y;
+                    sw.p[j] = (ti[u] << 1) | 1;
+                    sw.c[j] = cand;
+                }
+                sw.n += __popc(mo);
                 const bool seed = own && cand <= cutoff;
                 nseed += seed;
                 // only states with epsilon arcs enter the closure
-                st_f.push(seed && ((unsigned)e[u].x & EPS_FLAG), v, nf0, f0);
+                const bool fz = seed && ((unsigned)e[u].x & EPS_FLAG);
+                const unsigned mf = __ballot_sync(FULL, fz);
+                if (fz) {
+                    const int j = sf.n + __popc(mf & lt);
+                    sf.v[j] = v;
+                    sf.c[j] = cand;
+                }
+                sf.n += __popc(mf);
                 if (hist && seed) atomicAdd(wh + hist_bin(cand, best, width, inv_w), 1);
+                if (sw.n > SWW - 32) win_flush(sw, ntouched);
+                if (sf.n > SWW - 32) fr_flush(sf, nf0, f0);
             }
         }
-        st_t.flush(ntouched, tl);
-        st_f.flush(nf0, f0);
+        win_flush(sw, ntouched);
+        fr_flush(sf, nf0, f0);
         nseed = warp_sum(nseed);
         if (lane == 0 && nseed) atomicAdd(&lane_sm.nseed[par], (int)nseed);
         wend(1, t0);
@@ -676,12 +731,12 @@ struct Lane {
     // semantics (reference.py:160-192).
     __device__ bool epsilon(double cutoff, int frame) {
         const bool LAT = p.want_lattice;
-        StateRec *rec = L.rec;
+        unsigned long long *pk = L.pk;
         const unsigned round_id0 = lane_sm.round_id;
         unsigned round_id = round_id0;
         unsigned c_escan = 0, c_ecand = 0, c_front = 0;
-        unsigned *tl = touched();
-        int *ntouched = &lane_sm.ntouched[par];
+        unsigned *etl = etouched();
+        int *netouched = &lane_sm.netouched[par];
         const int bd = blockDim.x;
         bool ok = true;
         for (int r = 0;; r++) {
@@ -711,14 +766,13 @@ struct Lane {
                 for (int u = 0; u < EUNR; u++) {
                     const int k = k0 + u * bd;
                     v[u] = k < nf ? __ldcg(fs + k) : 0xFFFFFFFFu;
+                    c[u] = (r == 0 && k < nf) ? __ldcg(L.f0cost + cseg() + k) : 0.0;   // seeds carry their cost
                 }
 #pragma unroll
                 for (int u = 0; u < EUNR; u++) {
                     if (v[u] == 0xFFFFFFFFu) continue;
                     er[u] = gld2(g.erng + v[u]);
-                    if (r == 0) {
-                        c[u] = rld_f64(&rec[v[u]].cost);
-                    } else {
+                    if (r > 0) {
                         const ulonglong2 w2 = rld_u128(rprev + v[u]);
                         rst_u128(rprev + v[u], make_ulonglong2(~0ull, ~0ull));
                         c[u] = __longlong_as_double((long long)w2.y);
@@ -733,8 +787,8 @@ struct Lane {
                     if (!(c[u] <= cutoff)) continue;      // round-0 seeds above a max-active cutoff
                     c_front++;
                     if (LAT) {
-                        const double m = rld_f64(&rec[v[u]].minsnap);
-                        if (c[u] < m) rst_f64(&rec[v[u]].minsnap, c[u]);
+                        const double m = rld_f64(L.msnap + v[u]);
+                        if (c[u] < m) rst_f64(L.msnap + v[u], c[u]);
                     }
                     c_escan += er[u].y - er[u].x;
                     for (unsigned e = er[u].x; e < er[u].y; ++e) {
@@ -744,10 +798,10 @@ struct Lane {
                         c_ecand++;
                         const unsigned x = (unsigned)rr.x;
                         const unsigned long long word = pack_word(cand, (unsigned)rr.y);
-                        const unsigned long long old = atom_min_u64(&rec[x].pack, word);
-                        if (old == SENT) {
-                            const int sl = agg_append(ntouched);
-                            __stcg(tl + sl, x);
+                        const unsigned long long old = atom_min_u64(pk + x, word);
+                        if (old == SENT) {   // first reached by epsilon this frame
+                            const int sl = agg_append(netouched);
+                            __stcg(etl + sl, x);
                         }
                         if (old > word) {
                             // tag exchange issued before the winner CAS: both in flight together
@@ -763,7 +817,9 @@ struct Lane {
                 if (r > 0) {
 #pragma unroll
                     for (int u = 0; u < EUNR; u++)
-                        if (v[u] != 0xFFFFFFFFu) store_winner(&rec[v[u]], c[u], (int)(src[u] << 1));
+                        if (v[u] != 0xFFFFFFFFu)
+                            rst_u128(L.erec + v[u], make_ulonglong2((unsigned long long)__double_as_longlong(c[u]),
+                                                                    (unsigned long long)(unsigned)(src[u] << 1)));
                 }
             }
             wend(3, t0);
@@ -785,16 +841,18 @@ struct Lane {
     }
 
     // ---- aggregate + reset: frame token list at io.tok_*[tb ...]; returns count or -1 ----
-    // Warp-uniform loop over this CTA's touched list: ONE 32-byte record load
-    // per touched state.  A dropped state's word is reset at once; a kept state
-    // is staged per warp with everything its token needs, and a stage flush
-    // takes lane-wide token indices in bulk (one DSMEM counter atomic per flush),
-    // writes the token records (coalesced) and the state record in ONE 32-byte
-    // store (token index set, word reset).  Tokens whose predecessor is an
-    // epsilon source STATE go to this CTA's fix list; fix_preds() maps them to
-    // token indices during the next frame's emit.
+    // Warp-uniform loop over this CTA's emitting winners (payload read
+    // coalesced) and then its epsilon-reached states.  ONE scattered access per
+    // state does both the read of the final word and its reset (atom.exch to
+    // SENT).  A winner whose word survived keeps its payload; a state whose
+    // word an epsilon offer improved takes its cost / predecessor from `erec`.
+    // Kept states are staged per warp; a stage flush takes lane-wide token
+    // indices in bulk (one DSMEM counter atomic per flush), writes the token
+    // records coalesced and the states' token indices.  Tokens whose
+    // predecessor is an epsilon source STATE go to this CTA's fix list;
+    // fix_preds() maps them to token indices during the next frame's emit.
     struct TokStage {
-        double *cost, *msnap;
+        double *cost;
         unsigned *v, *arc, *key;
         int *pred;
         int n;
@@ -803,8 +861,7 @@ struct Lane {
         char *b = scratch();
         TokStage t;
         t.cost = reinterpret_cast<double *>(b);
-        t.msnap = t.cost + SWT;
-        t.v = reinterpret_cast<unsigned *>(t.msnap + SWT);
+        t.v = reinterpret_cast<unsigned *>(t.cost + SWT);
         t.arc = t.v + SWT;
         t.key = t.arc + SWT;
         t.pred = reinterpret_cast<int *>(t.key + SWT);
@@ -825,7 +882,6 @@ struct Lane {
         int base = 0;
         if (lane == 0) base = atomicAdd(&G.M->ntok[par], st.n);
         base = __shfl_sync(FULL, base, 0);
-        StateRec *rec = L.rec;
         for (int i0 = 0; i0 < st.n; i0 += 32) {
             const int i = i0 + lane;
             bool fx = false;
@@ -842,11 +898,9 @@ struct Lane {
                 __stcs(io.tok_pred + o, init ? -1 : pr);
                 if (p.collect_packs)
                     __stcs(io.tok_pack + o, ((unsigned long long)st.key[i] << 32) | st.arc[i]);
-                store_rec32(&rec[v], c, pr, idx, SENT, st.msnap[i]);
+                rst_i32(L.tokidx + v, idx);
                 fx = !init && (pr & 1) == 0;
-            } else if (i < st.n) {
-                rst_u64(&rec[st.v[i]].pack, SENT);   // over the arena: error raised after the barrier
-            }
+            }   // over the arena: the error is raised after the barrier (the word is already reset)
             sf.push(fx, (unsigned)idx, &lane_sm.nfix[par], fixes());
         }
         __syncwarp();
@@ -854,53 +908,51 @@ struct Lane {
     }
 
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = lane_sm.ntouched[par];
+        const int nt = lane_sm.ntouched[par], ne = lane_sm.netouched[par], ntot = nt + ne;
         const long long room = io.tok_cap - tb;
-        StateRec *rec = L.rec;
-        const unsigned *tl = touched();
+        unsigned long long *pk = L.pk;
+        const unsigned *tl = touched(), *etl = etouched();
+        const size_t cs = cseg();
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
         const unsigned lt = (1u << lane) - 1u;
         TokStage st = tok_stage();
         WStage sf = fix_stage();
         const unsigned long long t0 = wbegin();
-        // touched-list entries of the next batch are fetched one batch ahead
-        unsigned vn[AUNR];
-#pragma unroll
-        for (int u = 0; u < AUNR; u++) {
-            const int k = warp * 32 * AUNR + u * 32 + lane;
-            vn[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
-        }
-        for (int kb = warp * 32 * AUNR; kb < nt; kb += nw * 32 * AUNR) {
-            unsigned v[AUNR];
-#pragma unroll
-            for (int u = 0; u < AUNR; u++) {
-                v[u] = vn[u];
-                const int k = kb + nw * 32 * AUNR + u * 32 + lane;
-                vn[u] = k < nt ? __ldcg(tl + k) : 0xFFFFFFFFu;
+        for (int kb = warp * 32; kb < ntot; kb += nw * 32) {
+            const int k = kb + lane;
+            const bool valid = k < ntot, win = k < nt;
+            unsigned v = 0, a = 0;
+            int pr = 0;
+            double c = 0.0;
+            if (win) {
+                v = __ldcg(tl + k);
+                a = __ldcg(L.tarc + cs + k);
+                pr = __ldcg(L.tpred + cs + k);
+                c = __ldcg(L.tcost + cs + k);
+            } else if (valid) {
+                v = __ldcg(etl + (k - nt));
             }
-            RecView rv[AUNR];
-#pragma unroll
-            for (int u = 0; u < AUNR; u++)
-                if (v[u] != 0xFFFFFFFFu) rv[u] = load_rec32(&rec[v[u]]);
-#pragma unroll
-            for (int u = 0; u < AUNR; u++) {
-                const bool valid = v[u] != 0xFFFFFFFFu;
-                const bool init = valid && frame == 0 && (int)v[u] == g.start;
-                const bool keep = valid && (init || rv[u].cost <= cutoff);
-                if (valid && !keep) rst_u64(&rec[v[u]].pack, SENT);
-                const unsigned m = __ballot_sync(FULL, keep);
-                if (keep) {
-                    const int j = st.n + __popc(m & lt);
-                    st.v[j] = v[u];
-                    st.cost[j] = rv[u].cost;
-                    st.msnap[j] = rv[u].minsnap;
-                    st.arc[j] = (unsigned)rv[u].pack;
-                    st.key[j] = (unsigned)(rv[u].pack >> 32);
-                    st.pred[j] = rv[u].pred;
-                }
-                st.n += __popc(m);
-                if (st.n > SWT - 32) flush_tokens(st, sf, frame, tb, room);
+            unsigned long long x = SENT;
+            if (valid) x = atom_exch_u64(pk + v, SENT);
+            if (valid && (!win || x != pack_word(c, a))) {   // improved by an epsilon offer
+                const ulonglong2 er = rld_u128(L.erec + v);
+                c = __longlong_as_double((long long)er.x);
+                pr = (int)(unsigned)er.y;
+                a = (unsigned)x;
             }
+            const bool init = valid && frame == 0 && (int)v == g.start;
+            const bool keep = valid && (init || c <= cutoff);
+            const unsigned m = __ballot_sync(FULL, keep);
+            if (keep) {
+                const int j = st.n + __popc(m & lt);
+                st.v[j] = v;
+                st.cost[j] = c;
+                st.arc[j] = a;
+                st.key[j] = (unsigned)(x >> 32);
+                st.pred[j] = pr;
+            }
+            st.n += __popc(m);
+            if (st.n > SWT - 32) flush_tokens(st, sf, frame, tb, room);
         }
         flush_tokens(st, sf, frame, tb, room);
         sf.flush(&lane_sm.nfix[par], fixes());
@@ -930,7 +982,7 @@ struct Lane {
     }
 
     __device__ __forceinline__ bool kept(unsigned v, long long tb, int n, int &j) const {
-        j = rld_i32(&L.rec[v].tokidx);
+        j = rld_i32(L.tokidx + v);
         return j >= 0 && j < n && __ldcg(io.tok_state + tb + j) == v;
     }
 
@@ -959,8 +1011,8 @@ struct Lane {
             for (int j = G.gtid(); j < n; j += G.gstride()) {
                 const unsigned u = __ldcg(io.tok_state + tb + j);
                 const unsigned e0 = __ldg(g.eoff + u), e1 = __ldg(g.eoff + u + 1);
-                const double ms = rld_f64(&L.rec[u].minsnap);
-                rst_f64(&L.rec[u].minsnap, inf);
+                const double ms = rld_f64(L.msnap + u);
+                if (ms < inf) rst_f64(L.msnap + u, inf);
                 for (unsigned e = e0; e < e1; ++e) {
                     const int4 r = __ldg(g.eps + e);
                     int jv;
@@ -982,13 +1034,13 @@ struct Lane {
     // ---- error path: O(touched) reset of every per-state word this frame touched ----
     __device__ void reset_touched() {
         G.sync();
-        const int nt = lane_sm.ntouched[par];
-        const unsigned *tl = touched();
+        const int nt = lane_sm.ntouched[par], ne = lane_sm.netouched[par];
+        const unsigned *tl = touched(), *etl = etouched();
         const double inf = inf_d();
-        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
-            const unsigned v = __ldcg(tl + k);
-            rst_u64(&L.rec[v].pack, SENT);
-            rst_f64(&L.rec[v].minsnap, inf);
+        for (int k = threadIdx.x; k < nt + ne; k += blockDim.x) {
+            const unsigned v = k < nt ? __ldcg(tl + k) : __ldcg(etl + (k - nt));
+            rst_u64(L.pk + v, SENT);
+            rst_f64(L.msnap + v, inf);
             rst_u128(rpk(0) + v, make_ulonglong2(~0ull, ~0ull));
             rst_u128(rpk(1) + v, make_ulonglong2(~0ull, ~0ull));
         }
@@ -1001,7 +1053,7 @@ __device__ __forceinline__ void init_smem(unsigned round_ctr) {
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; q++) {
             sm.ntok[q] = sm.nlat[q] = 0;
-            sm.ntouched[q] = sm.ncand[q] = sm.nseed[q] = sm.nfix[q] = 0;
+            sm.ntouched[q] = sm.ncand[q] = sm.nseed[q] = sm.nfix[q] = sm.netouched[q] = 0;
             sm.best[q] = SENT;
         }
         sm.nfr[0] = sm.nfr[1] = sm.nfr[2] = 0;
@@ -1017,14 +1069,16 @@ __device__ __forceinline__ void init_smem(unsigned round_ctr) {
 template <int UNR>
 __device__ __forceinline__ void seed_start(Lane<UNR> &ln, const GraphDev &g, const LaneWs &L) {
     if (ln.G.leader()) {
-        StateRec *r = &L.rec[g.start];
-        __stcg(&r->pack, pack_word(0.0, 0u));
-        __stcg(&r->cost, 0.0);
-        __stcg(&r->pred, -1);
-        __stcg(ln.touched(), (unsigned)g.start);
+        __stcg(L.pk + g.start, pack_word(0.0, 0u));
+        const size_t k = 0;   // the rank-0 CTA's first emitting-winner slot
+        __stcg(L.touched + k, (unsigned)g.start);
+        __stcg(L.tcost + k, 0.0);
+        __stcg(L.tpred + k, -1);
+        __stcg(L.tarc + k, 0u);
         lane_sm.ntouched[0] = 1;
         if (g.has_eps) {
             __stcg(ln.front(0), (unsigned)g.start);
+            __stcg(L.f0cost + k, 0.0);
             lane_sm.nfr[0] = 1;
         }
     }
@@ -1211,7 +1265,7 @@ __device__ __forceinline__ void decode_one(const GraphDev &g, const Params &p, c
     const int bstate = partial ? sc : st;
     if (G.leader()) {
         const double total = partial ? bc : bt;
-        const int bidx = __ldcg(&L.rec[bstate].tokidx);
+        const int bidx = __ldcg(L.tokidx + bstate);
         io.out_i[2] = partial;
         io.out_i[3] = bidx;
         io.out_d[0] = total;
@@ -1598,11 +1652,13 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         for (int i = tid; i < n; i += blockDim.x) {
             const unsigned s = __ldcg(io.tok_state + i);
             const double c = __ldcg(io.tok_cost + i);
-            __stcg(&L.rec[s].pack, pack_word(c, 0u));
-            __stcg(&L.rec[s].cost, c);
-            __stcg(&L.rec[s].pred, -1);
-            __stcg(ln.touched() + i, s);
+            __stcg(L.pk + s, pack_word(c, 0u));
+            __stcg(L.touched + i, s);
+            __stcg(L.tcost + i, c);
+            __stcg(L.tarc + i, 0u);
+            __stcg(L.tpred + i, -1);
             __stcg(ln.front(0) + i, s);
+            __stcg(L.f0cost + i, c);
         }
         __syncthreads();
         if (tid == 0) { sm.ntouched[1] = n; sm.nfr[0] = n; }
@@ -1612,17 +1668,22 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
         }
     }
     __syncthreads();
-    const int nt = sm.ntouched[1];
-    const unsigned *tl = ln.touched();
-    for (int k = tid; k < nt; k += blockDim.x) {
-        const unsigned v = __ldcg(tl + k);
-        const double c = __ldcg(&L.rec[v].cost);
+    // the closure's states: emitting winners / seeds with their payload, then the
+    // epsilon-reached ones; the final word says whether epsilon improved a state
+    const int nt = sm.ntouched[1], ne = sm.netouched[1];
+    const unsigned *tl = ln.touched(), *etl = ln.etouched();
+    for (int k = tid; k < nt + ne; k += blockDim.x) {
+        const bool win = k < nt;
+        const unsigned v = win ? __ldcg(tl + k) : __ldcg(etl + (k - nt));
+        double c = win ? __ldcg(L.tcost + k) : 0.0;
+        const unsigned a = win ? __ldcg(L.tarc + k) : 0u;
+        const unsigned long long x = atom_exch_u64(L.pk + v, SENT);
+        if (!win || x != pack_word(c, a)) c = __ldcg(&L.erec[v].cost);
         if (c <= cutoff) {
             const int idx = agg_append(&sm.ntok[1]);
             __stcg(io.tok_state + n + idx, v);
             __stcg(io.tok_cost + n + idx, c);
         }
-        __stcg(&L.rec[v].pack, SENT);
     }
     __syncthreads();
     if (tid == 0) {
@@ -1643,6 +1704,11 @@ __global__ void widen_f32_kernel(const WidenJob *__restrict__ jobs) {
     const WidenJob J = jobs[blockIdx.y];
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < J.n; i += (long long)gridDim.x * blockDim.x)
         J.dst[i] = (double)__ldg(J.src + i);
+}
+
+__global__ void fill_f64(double *a, long long n, double v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        a[i] = v;
 }
 
 // Workspace initialisation: every state record idle (pack SENT, no token, minsnap +inf).
