@@ -918,22 +918,35 @@ struct Lane {
         TokStage st = tok_stage();
         WStage sf = fix_stage();
         const unsigned long long t0 = wbegin();
-        for (int kb = warp * 32; kb < ntot; kb += nw * 32) {
-            const int k = kb + lane;
-            const bool valid = k < ntot, win = k < nt;
-            unsigned v = 0, a = 0;
-            int pr = 0;
-            double c = 0.0;
-            if (win) {
+        // the next batch's list entries (and winner payloads) are fetched one batch ahead
+        auto fetch = [&](int k, unsigned &v, unsigned &a, int &pr, double &c) {
+            v = 0;
+            a = 0;
+            pr = 0;
+            c = 0.0;
+            if (k < nt) {
                 v = __ldcg(tl + k);
                 a = __ldcg(L.tarc + cs + k);
                 pr = __ldcg(L.tpred + cs + k);
                 c = __ldcg(L.tcost + cs + k);
-            } else if (valid) {
+            } else if (k < ntot) {
                 v = __ldcg(etl + (k - nt));
             }
-            unsigned long long x = SENT;
-            if (valid) x = atom_exch_u64(pk + v, SENT);
+        };
+        unsigned vn, an;
+        int prn;
+        double cn;
+        fetch(warp * 32 + lane, vn, an, prn, cn);
+        for (int kb = warp * 32; kb < ntot; kb += nw * 32) {
+            const int k = kb + lane;
+            const bool valid = k < ntot, win = k < nt;
+            unsigned v = vn, a = an;
+            int pr = prn;
+            double c = cn;
+            fetch(k + nw * 32, vn, an, prn, cn);
+            // read the final word and reset it in one atomic (a plain load followed
+            // by a store to the same word measured 4-5x slower for the whole kernel)
+            const unsigned long long x = valid ? atom_exch_u64(pk + v, SENT) : SENT;
             if (valid && (!win || x != pack_word(c, a))) {   // improved by an epsilon offer
                 const ulonglong2 er = rld_u128(L.erec + v);
                 c = __longlong_as_double((long long)er.x);
