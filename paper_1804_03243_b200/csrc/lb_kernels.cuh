@@ -944,8 +944,8 @@ struct Lane {
             int pr = prn;
             double c = cn;
             fetch(k + nw * 32, vn, an, prn, cn);
-            // read the final word and reset it in one atomic (a plain load followed
-            // by a store to the same word measured 4-5x slower for the whole kernel)
+            // read the final word and reset it in one atomic (issuing the next
+            // batch's exchanges a batch ahead measured no faster)
             const unsigned long long x = valid ? atom_exch_u64(pk + v, SENT) : SENT;
             if (valid && (!win || x != pack_word(c, a))) {   // improved by an epsilon offer
                 const ulonglong2 er = rld_u128(L.erec + v);
