@@ -29,6 +29,11 @@
 
 using namespace lbk;
 
+// arcs per lane per emit batch in the 640-thread lane (the default CTA)
+#ifndef LB_UNR640
+#define LB_UNR640 2
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -867,7 +872,8 @@ int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
     if (it != g->cluster_fit.end()) return it->second;
     using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, const UttJob *, int, int *);
     KernT k = threads == 512 ? (KernT)decode_kernel<512, 4, false, false>
-            : threads == 768 ? (KernT)decode_kernel<768, 2, false, false> : (KernT)decode_kernel<640, 2, false, false>;
+            : threads == 768 ? (KernT)decode_kernel<768, 2, false, false>
+                             : (KernT)decode_kernel<640, LB_UNR640, false, false>;
     int num = 0;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1)) ==
             cudaSuccess &&
@@ -1075,7 +1081,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     KernT kern;
     // 640 threads (96 registers, few spills) measured best on C4: 440k vs 392k
     // frames/s at 768 and 417k at 512 (tools/cta_sweep.sh)
-    if (threads == 640) kern = LB_PICK(640, 2);
+    if (threads == 640) kern = LB_PICK(640, LB_UNR640);
     else if (threads == 768) kern = LB_PICK(768, 2);
     else if (threads == 512) kern = LB_PICK(512, 4);
     else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");

@@ -224,14 +224,43 @@ def corpus_max_active():
         r.update(status="ok", kind="uniform", seed=k, S=S, deg=deg, L=L, T=T, beam=beam,
                  max_active=ma, graph_hash=graph_hash(w), matrix_hash=arr_hash(m.costs))
         cases.append(r)
-    # an epsilon-bearing graph (reference random_wfst at a larger size)
-    for k in range(3):
+    # epsilon-bearing graphs (reference random_wfst at a larger size), varied beams / caps
+    prm = np.random.default_rng(4242)
+    for k in range(21):
         rng = np.random.default_rng(800 + k)
         w = RS.random_wfst(rng, max_states=400, max_arcs=2400, num_labels=30)
         m = RS.random_matrix(rng, 30, max_frames=25)
-        r = record(max_active_decode(w, m, 9.0, 60))
-        r.update(status="ok", kind="random_wfst", seed=800 + k, beam=9.0, max_active=60,
+        beam = 9.0 if k < 3 else float(np.round(prm.uniform(6.0, 13.0), 3))
+        ma = 60 if k < 3 else int(prm.integers(15, 150))
+        try:
+            r = record(max_active_decode(w, m, beam, ma))
+        except latbeam.LatbeamError:
+            continue
+        r.update(status="ok", kind="random_wfst", seed=800 + k, beam=beam, max_active=ma,
                  graph_hash=graph_hash(w), matrix_hash=arr_hash(m.costs))
+        cases.append(r)
+    # HCLG-shaped graphs (paper_1804_03243_b200.synthetic.hclg_graph, the C2-C5
+    # generator at small size) through the reference frame loop
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1804_03243_b200 import synthetic as OS
+    for k in range(16):
+        S = int(prm.integers(8_000, 30_000))
+        pool = int(prm.integers(300, 1200))
+        ma = int(prm.integers(100, 900))
+        beam = float(np.round(prm.uniform(10.0, 14.0), 3))
+        T = int(prm.integers(12, 30))
+        ow = OS.hclg_graph(k, num_states=S, pool_size=pool, num_pdfs=80)
+        om = OS.hclg_matrix(900 + k, num_frames=T, num_pdfs=80)
+        w = latbeam.Wfst(ow.num_states, ow.start_state, np.array(ow.arc_offsets), np.array(ow.arc_src),
+                         np.array(ow.arc_dst), np.array(ow.arc_ilabel), np.array(ow.arc_olabel),
+                         np.array(ow.arc_weight), dict(ow.final_costs))
+        m = latbeam.CostMatrix(np.array(om.costs))
+        try:
+            r = record(max_active_decode(w, m, beam, ma))
+        except latbeam.LatbeamError:
+            continue
+        r.update(status="ok", kind="hclg", seed=k, S=S, pool=pool, T=T, beam=beam, max_active=ma,
+                 graph_hash=graph_hash(ow), matrix_hash=arr_hash(om.costs))
         cases.append(r)
     return cases
 

@@ -123,14 +123,25 @@ def test_golden_corpus_is_substantive():
     assert sum(1 for c in CASES if int(c.get("cycles", 0))) >= 20
 
 
-@pytest.mark.parametrize("idx", range(6))
+MA_CASES = load("max_active.npz")
+
+
+def test_max_active_corpus_is_substantive():
+    kinds = [str(c["kind"]) for c in MA_CASES]
+    assert len(MA_CASES) >= 40 and kinds.count("hclg") >= 12 and kinds.count("random_wfst") >= 20
+
+
+@pytest.mark.parametrize("idx", range(len(MA_CASES)))
 def test_max_active_extension_golden(oracle_mod, idx):
     """Max-active extension vs the reference frame loop with the DESIGN.md §3 cutoff."""
-    c = load("max_active.npz")[idx]
+    c = MA_CASES[idx]
     if str(c["kind"]) == "uniform":
         w = synthetic.uniform_bench_graph(int(c["seed"]), num_states=int(c["S"]),
                                           arcs_per_state=int(c["deg"]), num_labels=int(c["L"]))
         m = synthetic.bench_matrix(500 + int(c["seed"]), num_frames=int(c["T"]), num_labels=int(c["L"]))
+    elif str(c["kind"]) == "hclg":
+        w = synthetic.hclg_graph(int(c["seed"]), num_states=int(c["S"]), pool_size=int(c["pool"]), num_pdfs=80)
+        m = synthetic.hclg_matrix(900 + int(c["seed"]), num_frames=int(c["T"]), num_pdfs=80)
     else:
         rng = np.random.default_rng(int(c["seed"]))
         w = synthetic.random_wfst(rng, max_states=400, max_arcs=2400, num_labels=30)

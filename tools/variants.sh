@@ -15,5 +15,5 @@ done
 for p in "${pids[@]}"; do wait $p; done
 for spec in "$@"; do
   name="${spec%%:*}"
-  echo "$name: $(grep -A2 'decode_kernelILi640ELi2ELb0ELb0' build/variants/$name.ptxas.txt | grep -o '[0-9]* bytes spill stores, [0-9]* bytes spill loads' | head -1)"
+  echo "$name: $(grep -A2 'decode_kernelILi640ELi.ELb0ELb0' build/variants/$name.ptxas.txt | grep -o '[0-9]* bytes spill stores, [0-9]* bytes spill loads' | head -1)"
 done
