@@ -29,7 +29,10 @@
 
 using namespace lbk;
 
-// arcs per lane per emit batch in the 640-thread lane (the default CTA)
+// threads of the default lane CTA and its arcs per lane per emit batch
+#ifndef LB_LANE_NT
+#define LB_LANE_NT 640
+#endif
 #ifndef LB_UNR640
 #define LB_UNR640 2
 #endif
@@ -527,7 +530,7 @@ int validate_cfg(const lb_config *c) {
     if (c->max_active < 0) return set_err(LB_USAGE, "max_active must be >= 0");
     if (c->max_tokens_per_frame < 1) return set_err(LB_USAGE, "max_tokens_per_frame must be >= 1");
     if (c->max_lattice_arcs < 1) return set_err(LB_USAGE, "max_lattice_arcs must be >= 1");
-    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != 640 &&
+    if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != LB_LANE_NT &&
         c->threads_per_lane != 768)
         return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
     if (c->ctas_per_lane < 0 || c->ctas_per_lane > 8) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 8]");
@@ -873,7 +876,7 @@ int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
     using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, const UttJob *, int, int *);
     KernT k = threads == 512 ? (KernT)decode_kernel<512, 4, false, false>
             : threads == 768 ? (KernT)decode_kernel<768, 2, false, false>
-                             : (KernT)decode_kernel<640, LB_UNR640, false, false>;
+                             : (KernT)decode_kernel<LB_LANE_NT, LB_UNR640, false, false>;
     int num = 0;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1)) ==
             cudaSuccess &&
@@ -900,7 +903,7 @@ int max_coresident_clusters(lb_graph *g, int C, int threads, size_t dsm) {
 // staging decision of lb_decode_batch).
 void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched, int &C) {
     const bool lat = cfg->want_lattice != 0;
-    const int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 640;
+    const int threads = cfg->threads_per_lane ? cfg->threads_per_lane : LB_LANE_NT;
     // Mode: the frame-synchronous batched kernels (lb_batched.cuh, replayed as a
     // CUDA graph, lanes in 4 concurrent groups) spread every phase over all SMs
     // and win for small and medium batches (1 utterance: 17.8k vs 8.1k frames/s;
@@ -991,7 +994,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     tok_cap = std::min<int64_t>(tok_cap, (int64_t)1 << 31);
     const int64_t lat_cap = lat ? std::min<int64_t>(cfg->max_lattice_arcs, (int64_t)1 << 31) : 0;
     const int path_cap = 4 * tmax + 256;
-    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : 640;
+    int threads = cfg->threads_per_lane ? cfg->threads_per_lane : LB_LANE_NT;
     bool batched;
     int C;
     choose_mode(g, n, D, cfg, batched, C);
@@ -1081,7 +1084,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     KernT kern;
     // 640 threads (96 registers, few spills) measured best on C4: 440k vs 392k
     // frames/s at 768 and 417k at 512 (tools/cta_sweep.sh)
-    if (threads == 640) kern = LB_PICK(640, LB_UNR640);
+    if (threads == LB_LANE_NT) kern = LB_PICK(LB_LANE_NT, LB_UNR640);
     else if (threads == 768) kern = LB_PICK(768, 2);
     else if (threads == 512) kern = LB_PICK(512, 4);
     else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");

@@ -62,3 +62,13 @@ def test_cuda_binary_targets_sm100a():
     so = os.path.join(ROOT, "paper_1804_03243_b200", "liblatbeam_b200.so")
     blob = open(so, "rb").read()
     assert b"sm_100a" in blob
+
+
+def test_integration_stub_matches_header():
+    """INTEGRATION.md's ctypes lb_config stub lists every header field, in order."""
+    text = open(HEADER).read()
+    body = text[text.index("typedef struct {", text.index("lb_graph lb_graph;")):text.index("} lb_config;")]
+    fields = [n for _, n in re.findall(r"(double|int64_t|int32_t)\s+([a-z_]+);", body)]
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    stub = doc[doc.index("class lb_config"):doc.index("L.lb_graph_create.argtypes")]
+    assert re.findall(r'\("([a-z_]+)", C\.c_', stub) == fields
