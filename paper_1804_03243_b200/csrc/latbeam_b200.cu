@@ -20,6 +20,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX 3: ranges are free unless a profiler injects itself
+
 #include "../../include/latbeam_b200.h"
 #include "lb_kernels.cuh"
 #include "lb_lattice.cuh"
@@ -40,6 +42,16 @@ using namespace lbk;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the host-side stages of a call (nsys / ncu --nvtx show them):
+// staging, the decode launch(es), pruning, finalisation, readback.  The decode
+// phases inside the persistent kernel are timed on the device instead
+// (LB_PHASE_PROFILE=1, lb_result_phases).
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+};
 
 int set_err(int code, const std::string &msg) {
     g_err = msg;
@@ -959,6 +971,7 @@ std::vector<int32_t> lpt_order(int n, const int32_t *T) {
 int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const int32_t *T, int32_t D,
                 const lb_config *cfg, cudaStream_t st, lb_result *res, float h2d_ms, const int *d_ready = nullptr,
                 const RingDev *ring = nullptr, bool costs_f32 = false) {
+    Nvtx range_("lb.decode");
     const bool lat = cfg->want_lattice != 0;
     if (lat) {
         // size the arena for what the last lattice decode took, so a steady
@@ -1208,6 +1221,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
         }
         CK(cudaEventRecord(e1, st));
         if (lat) {
+            Nvtx rp("lb.prune");
             // one cluster per utterance, as wide as the GPU allows (portable max 8)
             const unsigned pc = (unsigned)std::max(1, std::min(8, g->sms / std::max(nw, 1)));
             cudaLaunchConfig_t lc = {};
@@ -1225,6 +1239,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
             res->launches++;
         }
         CK(cudaEventRecord(e2, st));
+        Nvtx rr("lb.readback+finalize");
         const int u0 = refill ? 0 : w0;
         CK(cudaMemcpyAsync(hi.data() + 8 * (size_t)u0, w.j_out_i + 8 * (size_t)u0, 8 * sizeof(int) * (size_t)nj,
                            cudaMemcpyDeviceToHost, st));
@@ -1330,6 +1345,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
 // log-likelihood H2D).
 int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T, int D, const lb_config *cfg,
                 int lanes, lb_result *res) {
+    Nvtx range_("lb.decode_ring");
     int tmax = 1;
     for (int i = 0; i < n; i++) tmax = std::max(tmax, (int)T[i]);
     const long long slot_doubles = ((long long)tmax * D + 15) & ~15ll;   // slots start on 128-byte lines
@@ -1469,6 +1485,7 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     if (S < 1 || A < 0 || start < 0 || start >= S) return set_err(LB_USAGE, "bad graph dimensions / start state");
     if (S >= (1ll << 31) || A >= (1ll << 32) - 1) return set_err(LB_USAGE, "graph too large for 32-bit ids");
     if (off[0] != 0 || off[S] != A) return set_err(LB_USAGE, "arc offsets must start at 0 and end at num_arcs");
+    Nvtx range_("lb_graph_create");
     std::unique_ptr<lb_graph> g(new lb_graph());
     g->device = device;
     g->S = S;
@@ -1596,6 +1613,7 @@ int64_t lb_graph_device_bytes(const lb_graph *g) { return g ? g->bytes : 0; }
 
 int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, const int32_t *T, int32_t D,
                     const lb_config *cfg, lb_result **out) {
+    Nvtx range_("lb_decode_batch");
     lb_graph *g = const_cast<lb_graph *>(gc);
     if (!g || !out) return set_err(LB_USAGE, "graph/out is NULL");
     *out = nullptr;
@@ -1806,6 +1824,7 @@ int lb_decode_batch_multi(const lb_graph *const *graphs, int32_t n_graphs, int32
     std::vector<int> rcs(n_graphs, LB_OK);
     std::vector<std::string> msgs(n_graphs);
     auto run = [&](int k) {
+        Nvtx rs("lb.shard");
         const auto &ix = idx[k];
         std::vector<const double *> c(ix.size());
         std::vector<int32_t> t(ix.size());
