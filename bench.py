@@ -458,8 +458,9 @@ def main(argv=None):
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
-    if os.path.exists(PROFILE_SUMMARY):
-        traffic = json.load(open(PROFILE_SUMMARY)).get("dram_bytes_per_launch")
+    if os.path.exists(PROFILE_SUMMARY):   # ncu --set full capture of the same kernel, per utterance-frame
+        prof = json.load(open(PROFILE_SUMMARY))
+        traffic = prof.get("dram_bytes_per_frame", 0) * frames_mine or prof.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": "decode_kernel", "alg_bytes_per_launch": alg_bytes / max(args.steps, 1),
