@@ -107,6 +107,12 @@ int lb_result_status(const lb_result *r, int32_t utt, int32_t *status, char *mes
                      int32_t message_len, char *bound, int32_t bound_len);
 int lb_result_best(const lb_result *r, int32_t utt, double *total_cost, int32_t *partial,
                    int64_t *path_len, int64_t *num_tokens, int64_t *num_lattice_arcs);
+/* All utterances at once: status[n], total_cost[n], partial[n], path_off[n+1]
+ * (prefix offsets of the best paths) and counters[n*8]; any pointer may be NULL.
+ * lb_result_paths writes every utterance's best path back to back (path_off). */
+int lb_result_bulk(const lb_result *r, int32_t *status, double *total_cost, int32_t *partial,
+                   int64_t *path_off, int64_t *counters);
+int lb_result_paths(const lb_result *r, int32_t *arcs);
 /* Best path as graph arc ids in forward order; words = olabels > 0, alignment
  * = (ilabel, frame) of the emitting hops (decoder.py:614-641). */
 int lb_result_path(const lb_result *r, int32_t utt, int32_t *arcs);

@@ -37,6 +37,8 @@ SIGNATURES = {
     "lb_decode_batch_multi": (C.c_int, [C.POINTER(PV), C.c_int32, C.c_int32, C.POINTER(PD), P32, C.c_int32,
                                         PV, C.POINTER(PV)]),
     "lb_shard_lpt": (C.c_int, [C.c_int32, P32, C.c_int32, P32]),
+    "lb_result_bulk": (C.c_int, [PV, P32, PD, P32, P64, P64]),
+    "lb_result_paths": (C.c_int, [PV, P32]),
     "lb_result_count": (C.c_int, [PV, P32]),
     "lb_result_status": (C.c_int, [PV, C.c_int32, P32, C.c_char_p, C.c_int32, C.c_char_p, C.c_int32]),
     "lb_result_best": (C.c_int, [PV, C.c_int32, PD, P32, P64, P64, P64]),

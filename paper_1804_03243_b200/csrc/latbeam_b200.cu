@@ -1957,6 +1957,34 @@ int lb_result_count(const lb_result *r, int32_t *n) {
     if (!r || utt < 0 || utt >= (int32_t)r->utts.size()) return set_err(LB_USAGE, "bad result/utterance"); \
     const UttHost &u = r->utts[utt];
 
+// Every utterance's scalar results in one call (the per-utterance getters cost a
+// foreign call each, which dominates the host side of a 4096-utterance batch).
+int lb_result_bulk(const lb_result *r, int32_t *status, double *total_cost, int32_t *partial, int64_t *path_off,
+                   int64_t *counters) {
+    if (!r) return set_err(LB_USAGE, "NULL result");
+    const size_t n = r->utts.size();
+    if (path_off) path_off[0] = 0;
+    for (size_t u = 0; u < n; u++) {
+        const UttHost &x = r->utts[u];
+        if (status) status[u] = x.status;
+        if (total_cost) total_cost[u] = x.total_cost;
+        if (partial) partial[u] = x.partial;
+        if (path_off) path_off[u + 1] = path_off[u] + (int64_t)x.path.size();
+        if (counters) std::memcpy(counters + 8 * u, x.counters, sizeof(x.counters));
+    }
+    return LB_OK;
+}
+
+int lb_result_paths(const lb_result *r, int32_t *arcs) {
+    if (!r || !arcs) return set_err(LB_USAGE, "NULL argument");
+    size_t o = 0;
+    for (const UttHost &x : r->utts) {
+        if (!x.path.empty()) std::memcpy(arcs + o, x.path.data(), 4 * x.path.size());
+        o += x.path.size();
+    }
+    return LB_OK;
+}
+
 int lb_result_status(const lb_result *r, int32_t utt, int32_t *status, char *msg, int32_t msg_len, char *bound,
                      int32_t bound_len) {
     UTT_OR_FAIL

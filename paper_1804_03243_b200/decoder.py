@@ -312,44 +312,57 @@ def result_timing(res) -> dict:
             "d2h_ms": f[3].value, "launches": nl.value}
 
 
+_COUNTER_NAMES = ("n_tokens", "n_scan", "n_cand", "eps_front", "eps_scan", "eps_cand", "n_next", "n_lat")
+
+
 def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, collect_timings, t0):
+    """DecodeResults in input order.  The scalar results and every best path come
+    back in two bulk calls (lb_result_bulk / lb_result_paths); words and
+    alignments are sliced from one vectorised label lookup."""
     L = _lib.lib()
     tm = result_timing(res)
+    n = len(mats)
+    status = np.zeros(n, dtype=np.int32)
+    total = np.zeros(n)
+    part = np.zeros(n, dtype=np.int32)
+    poff = np.zeros(n + 1, dtype=np.int64)
+    cnt = np.zeros((n, 8), dtype=np.int64)
+    _raise_status(L.lb_result_bulk(res, ptr(status, P32), ptr(total, PD), ptr(part, P32), ptr(poff, P64),
+                                   ptr(cnt, P64)), _lib.last_error())
+    paths = np.zeros(max(int(poff[-1]), 1), dtype=np.int32)
+    _raise_status(L.lb_result_paths(res, ptr(paths, P32)), _lib.last_error())
+    il_all = wfst.arc_ilabel[paths[:poff[-1]]]
+    ol_all = wfst.arc_olabel[paths[:poff[-1]]]
+    cnt_l = cnt.tolist()
+    total_l, part_l, status_l, poff_l = total.tolist(), part.tolist(), status.tolist(), poff.tolist()
     out = []
     msg = C.create_string_buffer(256)
     bound = C.create_string_buffer(64)
     st = C.c_int32()
-    tc = C.c_double()
-    part = C.c_int32()
     plen, ntok, nlat = C.c_int64(), C.c_int64(), C.c_int64()
-    cnt = np.zeros(8, dtype=np.int64)
+    tcd, prt = C.c_double(), C.c_int32()
     for u, m in enumerate(mats):
-        L.lb_result_status(res, u, C.byref(st), msg, 256, bound, 64)
-        L.lb_result_counters(res, u, ptr(cnt, P64))
-        counters = dict(zip(("n_tokens", "n_scan", "n_cand", "eps_front", "eps_scan", "eps_cand",
-                             "n_next", "n_lat"), cnt.tolist()))
-        if st.value != 0:
+        counters = dict(zip(_COUNTER_NAMES, cnt_l[u]))
+        if status_l[u] != 0:
+            L.lb_result_status(res, u, C.byref(st), msg, 256, bound, 64)
             try:
                 _raise_status(st.value, msg.value.decode(), bound.value.decode())
             except Exception as exc:   # noqa: BLE001 - boxed per utterance
                 out.append(exc)
             continue
-        L.lb_result_best(res, u, C.byref(tc), C.byref(part), C.byref(plen), C.byref(ntok),
-                         C.byref(nlat))
-        path = np.zeros(plen.value, dtype=np.int32)
-        L.lb_result_path(res, u, ptr(path, P32))
-        il = wfst.arc_ilabel[path].astype(np.int64)
-        ol = wfst.arc_olabel[path].astype(np.int64)
+        a, b = poff_l[u], poff_l[u + 1]
+        il = il_all[a:b]
+        ol = ol_all[a:b]
         words = ol[ol > 0].tolist()
         ils = il[il > 0].tolist()
-        alignment = list(zip(ils, range(len(ils))))
-        r = DecodeResult(words, alignment, float(tc.value), bool(part.value), None, None, None,
-                         None, counters)
+        r = DecodeResult(words, list(zip(ils, range(len(ils)))), total_l[u], bool(part_l[u]), None, None,
+                         None, None, counters)
         if want_lattice:
             r.lattice = _final_lattice(res, u, m.shape[0])
             if not cfg.keep_work_lattice:
                 r.work_lattice = LazyWorkLattice(_work_thunk(wfst, m, cfg))
         if collect_frame_packs or (want_lattice and cfg.keep_work_lattice):
+            L.lb_result_best(res, u, C.byref(tcd), C.byref(prt), C.byref(plen), C.byref(ntok), C.byref(nlat))
             try:
                 _attach_lattice(r, wfst, res, u, m, cfg, ntok.value, nlat.value,
                                 want_lattice and cfg.keep_work_lattice, collect_frame_packs)
