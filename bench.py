@@ -318,10 +318,11 @@ def measure_configs(graph_c2, all_configs: bool) -> dict:
     return res
 
 
-def c5_batch_roofline(g5, n_utts: int = 128, lanes: int = 64) -> dict:
+def c5_batch_roofline(g5, n_utts: int = 512, lanes: int = 64) -> dict:
     """C5 (50M arcs, ~1000 epsilon hubs of in-degree ~8.5k, beam 16, max-active
-    20k) as a multi-utterance job: HBM-resident costs, 64 refilling lanes; the
-    decode kernel's algorithmic bytes over its event time."""
+    20k) as a multi-utterance job (512 utterances cycling through 16 distinct
+    matrices): HBM-resident costs, 64 refilling lanes; the decode kernel's
+    algorithmic bytes over its event time."""
     import torch
 
     import paper_1804_03243_b200 as lb

@@ -131,3 +131,22 @@ def test_c5_stress_utterance(oracle_mod):
                            max_active=d["max_active"], want_lattice=False)
     check_pair(got, ref, d["lattice_beam"], want_lattice=False)
     assert ref.counters["eps_scan"] > 0
+
+
+def test_c4_ragged_refill_full_graph(oracle_mod):
+    """C4's graph with a ragged job larger than the lane count: 192 utterances,
+    T ~ U[100, 500], 64 lanes -> one refilling launch (44 two-CTA + 20 three-CTA
+    lanes on one queue) fed through the streamed pinned ring; every total cost and
+    work counter equals the threaded oracle, in input order."""
+    w = graph("C4")
+    d = synthetic.CONFIGS["C4"]["decode"]
+    rng = np.random.default_rng(404)
+    mats = [np.ascontiguousarray(synthetic.hclg_matrix(5000 + u, num_frames=int(rng.integers(100, 501))).costs)
+            for u in range(192)]
+    tc, st, cnt = oracle_mod.decode_batch_mt(w, mats, d["beam"], max_active=d["max_active"])
+    res = lb.decode_batch(w, mats, lb.DecodeConfig(beam=d["beam"], max_active=d["max_active"], lanes=64),
+                          want_lattice=False)
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()
+    for r, c in zip(res, cnt):
+        assert _counters(r) == [c[0], c[1], c[6]]
