@@ -84,6 +84,11 @@ struct __align__(32) StateRec {
 #ifndef LB_NO_L2HINT
 #define LB_L2HINT 1
 #endif
+// the secondary per-state arrays (token index, epsilon winners / records, round
+// tags) take the same evict-last hint unless LB_SEC_NOHINT (an experiment knob)
+#if defined(LB_L2HINT) && !defined(LB_SEC_NOHINT)
+#define LB_SECHINT 1
+#endif
 #ifdef LB_L2HINT
 __device__ __forceinline__ unsigned long long l2_pol() {
     unsigned long long p;
@@ -106,7 +111,7 @@ __device__ __forceinline__ double rld_f64(const double *a) {
 }
 __device__ __forceinline__ int rld_i32(const int *a) {
     int v;
-#ifdef LB_L2HINT
+#ifdef LB_SECHINT
     asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(l2_pol()));
 #else
     v = __ldcg(a);
@@ -125,7 +130,7 @@ __device__ __forceinline__ void rst_f64(double *a, double v) {
 }
 __device__ __forceinline__ ulonglong2 rld_u128(const void *a) {
     ulonglong2 v;
-#ifdef LB_L2HINT
+#ifdef LB_SECHINT
     asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(a), "l"(l2_pol()));
 #else
     v = __ldcg(reinterpret_cast<const ulonglong2 *>(a));
@@ -133,7 +138,7 @@ __device__ __forceinline__ ulonglong2 rld_u128(const void *a) {
     return v;
 }
 __device__ __forceinline__ void rst_u128(void *a, ulonglong2 v) {
-#ifdef LB_L2HINT
+#ifdef LB_SECHINT
     asm volatile("st.global.cg.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(a), "l"(v.x), "l"(v.y), "l"(l2_pol()) : "memory");
 #else
     __stcg(reinterpret_cast<ulonglong2 *>(a), v);
@@ -389,7 +394,7 @@ __device__ __forceinline__ unsigned long long atom_min_u64(unsigned long long *a
 }
 __device__ __forceinline__ unsigned atom_exch_u32(unsigned *a, unsigned v) {
     unsigned o;
-#ifdef LB_L2HINT
+#ifdef LB_SECHINT
     asm volatile("atom.relaxed.gpu.global.exch.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(l2_pol()) : "memory");
 #else
     asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(a), "r"(v) : "memory");
@@ -399,7 +404,7 @@ __device__ __forceinline__ unsigned atom_exch_u32(unsigned *a, unsigned v) {
 
 __device__ __forceinline__ unsigned long long atom_exch_u64(unsigned long long *a, unsigned long long v) {
     unsigned long long o;
-#ifdef LB_L2HINT
+#if defined(LB_L2HINT) && defined(LB_EXCH_HINT)
     asm volatile("atom.relaxed.gpu.global.exch.L2::cache_hint.b64 %0, [%1], %2, %3;" : "=l"(o) : "l"(a), "l"(v), "l"(l2_pol()) : "memory");
 #else
     asm volatile("atom.relaxed.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(a), "l"(v) : "memory");
@@ -407,7 +412,7 @@ __device__ __forceinline__ unsigned long long atom_exch_u64(unsigned long long *
     return o;
 }
 __device__ __forceinline__ void rst_i32(int *a, int v) {
-#ifdef LB_L2HINT
+#ifdef LB_SECHINT
     asm volatile("st.global.cg.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_pol()) : "memory");
 #else
     __stcg(a, v);

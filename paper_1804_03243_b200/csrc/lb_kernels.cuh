@@ -135,6 +135,15 @@ __device__ __forceinline__ void cl_argmin(double &v, int &s, const Grp &G) {
 // cost[]) receives one batch; the batch loop is warp-uniform, so f may use
 // full-mask warp collectives.
 constexpr int WMAP = 512;
+// winner payload lists (written by winners, read once by aggregate): streamed
+// with evict-first under LB_PAY_EF (an experiment knob), L2-normal otherwise
+#ifdef LB_PAY_EF
+#define PAY_ST __stcs
+#define PAY_LD __ldcs
+#else
+#define PAY_ST __stcg
+#define PAY_LD __ldcg
+#endif
 template <int UNR, class F>
 __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, int gwarp, int gnw,
                                                            const unsigned *ts, const double *tc, int n,
@@ -537,10 +546,10 @@ struct Lane {
         base = __shfl_sync(FULL, base, 0);
         const size_t o = cseg() + base;
         for (int i = threadIdx.x & 31; i < st.n; i += 32) {
-            __stcg(L.touched + o + i, st.v[i]);
-            __stcg(L.tarc + o + i, st.a[i]);
-            __stcg(L.tpred + o + i, st.p[i]);
-            __stcg(L.tcost + o + i, st.c[i]);
+            PAY_ST(L.touched + o + i, st.v[i]);
+            PAY_ST(L.tarc + o + i, st.a[i]);
+            PAY_ST(L.tpred + o + i, st.p[i]);
+            PAY_ST(L.tcost + o + i, st.c[i]);
         }
         __syncwarp();
         st.n = 0;
@@ -925,10 +934,10 @@ struct Lane {
             pr = 0;
             c = 0.0;
             if (k < nt) {
-                v = __ldcg(tl + k);
-                a = __ldcg(L.tarc + cs + k);
-                pr = __ldcg(L.tpred + cs + k);
-                c = __ldcg(L.tcost + cs + k);
+                v = PAY_LD(tl + k);
+                a = PAY_LD(L.tarc + cs + k);
+                pr = PAY_LD(L.tpred + cs + k);
+                c = PAY_LD(L.tcost + cs + k);
             } else if (k < ntot) {
                 v = __ldcg(etl + (k - nt));
             }

@@ -333,8 +333,16 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
     _raise_status(L.lb_result_paths(res, ptr(paths, P32)), _lib.last_error())
     il_all = wfst.arc_ilabel[paths[:poff[-1]]]
     ol_all = wfst.arc_olabel[paths[:poff[-1]]]
+    # words / emitting ilabels of every utterance from one mask each, split at the
+    # utterances' boundaries in the compacted arrays
+    wmask, imask = ol_all > 0, il_all > 0
+    wcut = np.concatenate(([0], np.cumsum(wmask)))[poff]
+    icut = np.concatenate(([0], np.cumsum(imask)))[poff]
+    words_all = ol_all[wmask].tolist()
+    ils_all = il_all[imask].tolist()
+    wcut_l, icut_l = wcut.tolist(), icut.tolist()
     cnt_l = cnt.tolist()
-    total_l, part_l, status_l, poff_l = total.tolist(), part.tolist(), status.tolist(), poff.tolist()
+    total_l, part_l, status_l = total.tolist(), part.tolist(), status.tolist()
     out = []
     msg = C.create_string_buffer(256)
     bound = C.create_string_buffer(64)
@@ -350,13 +358,9 @@ def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, col
             except Exception as exc:   # noqa: BLE001 - boxed per utterance
                 out.append(exc)
             continue
-        a, b = poff_l[u], poff_l[u + 1]
-        il = il_all[a:b]
-        ol = ol_all[a:b]
-        words = ol[ol > 0].tolist()
-        ils = il[il > 0].tolist()
-        r = DecodeResult(words, list(zip(ils, range(len(ils)))), total_l[u], bool(part_l[u]), None, None,
-                         None, None, counters)
+        ils = ils_all[icut_l[u]:icut_l[u + 1]]
+        r = DecodeResult(words_all[wcut_l[u]:wcut_l[u + 1]], list(zip(ils, range(len(ils)))), total_l[u],
+                         bool(part_l[u]), None, None, None, None, counters)
         if want_lattice:
             r.lattice = _final_lattice(res, u, m.shape[0])
             if not cfg.keep_work_lattice:
