@@ -13,6 +13,7 @@ CUDA device every entry point raises DeviceError.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import math
 import threading
 import time
@@ -318,7 +319,20 @@ _COUNTER_NAMES = ("n_tokens", "n_scan", "n_cand", "eps_front", "eps_scan", "eps_
 def collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, collect_timings, t0):
     """DecodeResults in input order.  The scalar results and every best path come
     back in two bulk calls (lb_result_bulk / lb_result_paths); words and
-    alignments are sliced from one vectorised label lookup."""
+    alignments are sliced from one vectorised label lookup.  The cyclic garbage
+    collector is paused while the results are built: a 4096-utterance batch
+    allocates ~1.2M alignment tuples, and the collector's passes over them cost
+    twice the construction itself."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        return _collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, collect_timings, t0)
+    finally:
+        if was:
+            gc.enable()
+
+
+def _collect_results(wfst, res, mats, cfg, want_lattice, collect_frame_packs, collect_timings, t0):
     L = _lib.lib()
     tm = result_timing(res)
     n = len(mats)
