@@ -226,9 +226,10 @@ constexpr size_t ACROW_SMEM_MAX = 48 * 1024;   // acoustic rows up to 6144 pdfs 
 constexpr int SWW = 96;   // winners stages: touched {v, arc, pred, cost} and round-0 frontier {v, cost}
 constexpr int WSCR = (SWT * 32 + SW * 4) > SWW * 32 ? (SWT * 32 + SW * 4) : SWW * 32;
 static_assert(SWW * 20 + SWW * 12 <= WSCR, "winners stages fit the warp scratch");
-inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem) {
+// `row_pf`: two row buffers (the next frame's row is prefetched, Lane::row_async).
+inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem, bool row_pf = false) {
     const size_t nw = (size_t)threads / 32;
-    return (acrow_smem ? (size_t)D * 8 : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
+    return (acrow_smem ? (size_t)D * 8 * (row_pf ? 2 : 1) : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
 }
 constexpr int CAND_CHUNK = 256;   // Lane::CCH
 
@@ -279,7 +280,7 @@ struct Lane {
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
                     const Grp &G_, double *)
         : g(g_), p(p_), L(L_), io(io_), G(G_), row(nullptr), par(0) {}
-    __device__ __forceinline__ int acrow_doubles() const { return p.acrow_smem ? p.D : 0; }
+    __device__ __forceinline__ int acrow_doubles() const { return p.acrow_smem ? p.D * (p.row_pf ? 2 : 1) : 0; }
     __device__ __forceinline__ int *own_all() const { return reinterpret_cast<int *>(lane_dyn + acrow_doubles()); }
     __device__ __forceinline__ char *scratch_all() const {
         return reinterpret_cast<char *>(own_all() + (blockDim.x >> 5) * WMAP);
@@ -322,7 +323,32 @@ struct Lane {
     __device__ __forceinline__ int *wmap() const { return own_all() + (threadIdx.x >> 5) * WMAP; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
-        return p.acrow_smem ? lane_dyn[il - 1] : __dmul_rn(__ldg(row + il - 1), p.scale);
+        // with the row prefetch, frame t's row (t-1) sits in buffer (t-1)&1 = par^1
+        return p.acrow_smem ? lane_dyn[(p.row_pf ? (par ^ 1) * p.D : 0) + il - 1]
+                            : __dmul_rn(__ldg(row + il - 1), p.scale);
+    }
+
+    // Next-frame row prefetch (p.row_pf; f64 rows of even D, 16-byte aligned,
+    // device-resident or streamed ring): frame t's emit reads row t-1 from buffer
+    // (t-1)&1 while row t is already in flight into the other buffer with
+    // cp.async (L2 only, .cg, so a ring slot's stale line can never come from L1).
+    // Each thread scales exactly the doubles it copied, after its own wait; the
+    // barrier before emit publishes them.
+    __device__ __forceinline__ void row_async(const double *r, int buf) {
+        const unsigned base = (unsigned)__cvta_generic_to_shared(lane_dyn + buf * p.D);
+        const int chunks = p.D >> 1;
+        for (int q = threadIdx.x; q < chunks; q += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + 16u * q), "l"(r + 2 * q) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __device__ __forceinline__ void row_finish(int buf) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        double *d = lane_dyn + buf * p.D;
+        const int chunks = p.D >> 1;
+        for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
+            d[2 * q] = __dmul_rn(d[2 * q], p.scale);
+            d[2 * q + 1] = __dmul_rn(d[2 * q + 1], p.scale);
+        }
     }
 
     __device__ __forceinline__ void set_error(int code, int frame, long long aux) const {
@@ -1170,10 +1196,16 @@ __device__ __forceinline__ void decode_one(const GraphDev &g, const Params &p, c
         if (G.leader()) sm.c_tok += np;
         ln.par = t & 1;
         reset_done = false;
-        ln.load_row(p.costs_f32 ? reinterpret_cast<const double *>(reinterpret_cast<const float *>(io.costs) +
-                                                                   (long long)(t - 1) * p.D)
-                                : io.costs + (long long)(t - 1) * p.D,
-                    t - 1);
+        if (p.row_pf) {   // row t-1 was requested during frame t-1 (or now, at t = 1)
+            if (t == 1) ln.row_async(io.costs, 0);
+            ln.row_finish((t - 1) & 1);
+            if (t < T) ln.row_async(io.costs + (long long)t * p.D, t & 1);
+        } else {
+            ln.load_row(p.costs_f32 ? reinterpret_cast<const double *>(reinterpret_cast<const float *>(io.costs) +
+                                                                       (long long)(t - 1) * p.D)
+                                    : io.costs + (long long)(t - 1) * p.D,
+                        t - 1);
+        }
         if (g.has_eps) ln.fix_preds((t - 1) & 1, t - 1, tbp, np);
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff, t);
