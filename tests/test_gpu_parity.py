@@ -625,3 +625,31 @@ def test_work_lattice_by_default():
     assert lazy.work_lattice.num_frames == eager.work_lattice.num_frames
     assert [f.states.tolist() for f in lazy.work_lattice.frames] == [f.states.tolist() for f in eager.work_lattice.frames]
     assert lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0), want_lattice=False).work_lattice is None
+
+
+def test_row_prefetch_and_its_fallbacks(oracle_mod, monkeypatch):
+    """The next-frame row prefetch (16-byte cp.async of f64 rows) and the paths
+    that cannot use it -- matrices only 8-byte aligned in HBM, LB_NO_ROWPF --
+    all equal the oracle."""
+    import torch
+
+    from paper_1804_03243_b200.resident import decode_batch_resident
+    w = synthetic.hclg_graph(13, num_states=60_000, pool_size=1500, num_pdfs=300)
+    mats = _ragged_batch(24, 7500)
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=600)
+    assert all(st == 0)
+    cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=5)
+    aligned = [torch.from_numpy(m.copy()).cuda() for m in mats]
+    flat = torch.zeros(sum(m.size for m in mats) + 1, dtype=torch.float64, device="cuda")
+    views, o = [], 1                                     # every matrix starts 8 bytes off a 16-byte line
+    for m in mats:
+        v = flat[o:o + m.size].view(m.shape)
+        v.copy_(torch.from_numpy(m))
+        views.append(v)
+        o += m.size
+    for tens in (aligned, views):
+        outs, _ = decode_batch_resident(w, tens, cfg)
+        assert [x["total_cost"] for x in outs] == tc.tolist()
+    monkeypatch.setenv("LB_NO_ROWPF", "1")
+    outs, _ = decode_batch_resident(w, aligned, cfg)
+    assert [x["total_cost"] for x in outs] == tc.tolist()
