@@ -199,6 +199,18 @@ int lb_prune_lattice(int32_t device, int32_t t, const int64_t *frame_off, const 
                      const double *terminus, double lattice_beam, uint8_t *status, double *extra,
                      double *node_extra);
 
+/* finalize_lattice (lattice.py:537-598) of a work lattice handed in by the
+ * caller, on the device: its n LIVE arcs with node keys (frame << 32) | token
+ * index (from_key / to_key), labels and costs; the start token's index in frame
+ * 0; the last frame and, unless partial, its tokens' final costs (+inf = not
+ * final).  The FinalLattice comes back as a one-utterance result (status
+ * DecodeFailure when nothing survives or the start is cut off), read with
+ * lb_result_final_lattice / lb_result_final_arrays64. */
+int lb_finalize_lattice(int32_t device, int64_t n, const uint64_t *from_key, const uint64_t *to_key,
+                        const int32_t *ilabel, const int32_t *olabel, const double *graph_cost,
+                        const double *acoustic_cost, int64_t start_idx, int32_t last_frame, int32_t partial,
+                        int64_t n_final_costs, const double *final_costs, lb_result **out);
+
 /* Single-op surfaces (decoder.py:373-435): one frontier on device.
  * out_* need room for num_states entries; *n_out receives the count. */
 int lb_expand_emitting(const lb_graph *g, const int32_t *states, const double *costs, int64_t n,

@@ -59,6 +59,8 @@ SIGNATURES = {
                                     P64, PD, PD, C.c_char_p, C.c_int64]),
     "lb_prune_lattice": (C.c_int, [C.c_int32, C.c_int32, P64, PD, P64, P32, P32, C.POINTER(C.c_uint8), PD, PD,
                                    PD, C.c_double, C.POINTER(C.c_uint8), PD, PD]),
+    "lb_finalize_lattice": (C.c_int, [C.c_int32, C.c_int64, PU64, PU64, P32, P32, PD, PD, C.c_int64, C.c_int32,
+                                      C.c_int32, C.c_int64, PD, C.POINTER(PV)]),
     "lb_expand_emitting": (C.c_int, [PV, P32, PD, C.c_int64, PD, C.c_int32, C.c_double, P32, PD,
                                      P64, PD]),
     "lb_expand_nonemitting": (C.c_int, [PV, P32, PD, C.c_int64, C.c_double, P32, PD, P64]),

@@ -2302,6 +2302,158 @@ int64_t lb_lattice_text(int64_t num_nodes, int64_t start, int64_t n_final, const
     return total;
 }
 
+// finalize_lattice (lattice.py:537-598) on the device for a host work lattice:
+// the caller passes its LIVE arcs with node keys (frame << 32) | token index;
+// nodes are the sorted unique keys (dense ids), arcs come back in the canonical
+// np.lexsort((ac, g, ol, il, to, from)) order, final nodes are the last frame's
+// nodes with a finite final cost.  The result is read with lb_result_final_*.
+int lb_finalize_lattice(int32_t device, int64_t n, const uint64_t *from_key, const uint64_t *to_key,
+                        const int32_t *ilabel, const int32_t *olabel, const double *graph_cost,
+                        const double *acoustic_cost, int64_t start_idx, int32_t last_frame, int32_t partial,
+                        int64_t n_final_costs, const double *final_costs, lb_result **out) {
+    if (!out) return set_err(LB_USAGE, "out is NULL");
+    *out = nullptr;
+    if (n < 0 || last_frame < 0) return set_err(LB_USAGE, "bad lattice dimensions");
+    if (n >= (1ll << 31)) return set_err(LB_USAGE, "lattice too large");
+    std::unique_ptr<lb_result> res(new lb_result());
+    res->utts.resize(1);
+    UttHost &u = res->utts[0];
+    u.status = LB_OK;
+    u.has_final = true;
+    if (n == 0) {
+        u.status = LB_DECODE_FAILURE;
+        u.msg = "no lattice arcs survived pruning";
+        *out = res.release();
+        return LB_OK;
+    }
+    CK(cudaSetDevice(device));
+    cudaStream_t st = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<void *> bufs;
+    struct Free {
+        std::vector<void *> &b;
+        cudaStream_t s;
+        ~Free() {
+            for (void *p : b) cudaFree(p);
+            cudaStreamDestroy(s);
+        }
+    } fr{bufs, st};
+    auto A = [&](auto **dp, size_t cnt) -> cudaError_t {
+        cudaError_t e = dalloc(dp, cnt);
+        if (e == cudaSuccess) bufs.push_back((void *)*dp);
+        return e;
+    };
+    const size_t m = (size_t)n;
+    unsigned long long *fk, *tk, *nodes0, *nodes1, *k64a, *k64b, *count;
+    unsigned *il, *ol, *fid, *tid, *k32a, *k32b;
+    double *gc, *ac, *o_g, *o_ac, *fcs, *fc_in;
+    int *perm0, *perm1, *o_from, *o_to, *o_il, *o_ol, *n_unique;
+    long long *fids;
+    CK(A(&fk, m)); CK(A(&tk, m)); CK(A(&nodes0, 2 * m)); CK(A(&nodes1, 2 * m)); CK(A(&k64a, m)); CK(A(&k64b, m));
+    CK(A(&count, 1)); CK(A(&il, m)); CK(A(&ol, m)); CK(A(&fid, m)); CK(A(&tid, m)); CK(A(&k32a, m)); CK(A(&k32b, m));
+    CK(A(&gc, m)); CK(A(&ac, m)); CK(A(&o_g, m)); CK(A(&o_ac, m)); CK(A(&fcs, 2 * m));
+    CK(A(&fc_in, (size_t)std::max<int64_t>(n_final_costs, 1)));
+    CK(A(&perm0, m)); CK(A(&perm1, m)); CK(A(&o_from, m)); CK(A(&o_to, m)); CK(A(&o_il, m)); CK(A(&o_ol, m));
+    CK(A(&n_unique, 1)); CK(A(&fids, 2 * m));
+    CK(cudaMemcpyAsync(fk, from_key, 8 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(tk, to_key, 8 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(nodes0, from_key, 8 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(nodes0 + m, to_key, 8 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(il, ilabel, 4 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ol, olabel, 4 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(gc, graph_cost, 8 * m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ac, acoustic_cost, 8 * m, cudaMemcpyHostToDevice, st));
+    if (n_final_costs > 0 && final_costs)
+        CK(cudaMemcpyAsync(fc_in, final_costs, 8 * (size_t)n_final_costs, cudaMemcpyHostToDevice, st));
+    // CUB scratch for the largest sort / unique
+    size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, t1, nodes0, nodes1, (int)(2 * m), 0, 64, st));
+    CK(cub::DeviceSelect::Unique(nullptr, t2, nodes1, nodes0, n_unique, (int)(2 * m), st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k64a, k64b, perm0, perm1, (int)m, 0, 64, st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t4, k32a, k32b, perm0, perm1, (int)m, 0, 32, st));
+    size_t tcap = std::max(std::max(t1, t2), std::max(t3, t4));
+    void *temp = nullptr;
+    CK(A((char **)&temp, tcap));
+    const int nblk = 148 * 4;
+    CK(cub::DeviceRadixSort::SortKeys(temp, tcap, nodes0, nodes1, (int)(2 * m), 0, 64, st));
+    tcap = std::max(std::max(t1, t2), std::max(t3, t4));
+    CK(cub::DeviceSelect::Unique(temp, tcap, nodes1, nodes0, n_unique, (int)(2 * m), st));
+    int nn = 0;
+    CK(cudaMemcpyAsync(&nn, n_unique, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fl_node_ids<<<nblk, 256, 0, st>>>(fk, tk, (long long)m, nodes0, nn, fid, tid);
+    fl_iota<<<nblk, 256, 0, st>>>(perm0, (long long)m);
+    int *pa = perm0, *pb = perm1;
+    for (int pass = 0; pass < 6; pass++) {   // np.lexsort((ac, g, ol, il, to, from)): last key primary
+        tcap = std::max(std::max(t1, t2), std::max(t3, t4));
+        if (pass < 2) {
+            fl_gather_u64<<<nblk, 256, 0, st>>>(pass == 0 ? ac : gc, pa, (long long)m, k64a);
+            CK(cub::DeviceRadixSort::SortPairs(temp, tcap, k64a, k64b, pa, pb, (int)m, 0, 64, st));
+        } else {
+            const unsigned *srcp = pass == 2 ? ol : pass == 3 ? il : pass == 4 ? tid : fid;
+            fl_gather_u32<<<nblk, 256, 0, st>>>(srcp, pa, (long long)m, k32a);
+            CK(cub::DeviceRadixSort::SortPairs(temp, tcap, k32a, k32b, pa, pb, (int)m, 0, 32, st));
+        }
+        std::swap(pa, pb);
+    }
+    fl_emit<<<nblk, 256, 0, st>>>(pa, (long long)m, fid, tid, il, ol, gc, ac, o_from, o_to, o_il, o_ol, o_g, o_ac);
+    CK(cudaMemsetAsync(count, 0, 8, st));
+    fl_finals_given<<<nblk, 256, 0, st>>>(nodes0, nn, last_frame, fc_in, n_final_costs, partial, fids, fcs, count);
+    CK(cudaGetLastError());
+    unsigned long long nf = 0;
+    CK(cudaMemcpyAsync(&nf, count, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // host copies (a private arena owned by the result)
+    auto arena = std::make_shared<HostArena>();
+    const size_t bytes = 8 * (size_t)nn + 32 * m + 8 * 256;
+    CK(cudaHostAlloc((void **)&arena->p, bytes, cudaHostAllocDefault));
+    arena->cap = bytes;
+    auto take = [&](auto &span, size_t cnt) {
+        using T = typename std::remove_reference<decltype(*span.p)>::type;
+        span.p = reinterpret_cast<T *>(arena->p + arena->used);
+        span.n = cnt;
+        arena->used += (cnt * sizeof(T) + 255) & ~(size_t)255;
+    };
+    take(u.fl_nodes, (size_t)nn);
+    take(u.fl_from, m); take(u.fl_to, m); take(u.fl_il, m); take(u.fl_ol, m); take(u.fl_g, m); take(u.fl_ac, m);
+    u.fl_arena = arena;
+    CK(cudaMemcpyAsync(u.fl_nodes.data(), nodes0, 8 * (size_t)nn, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_from.data(), o_from, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_to.data(), o_to, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_il.data(), o_il, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_ol.data(), o_ol, 4 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_g.data(), o_g, 8 * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(u.fl_ac.data(), o_ac, 8 * m, cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> ids(nf);
+    std::vector<double> fcv(nf);
+    CK(cudaMemcpyAsync(ids.data(), fids, 8 * nf, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fcv.data(), fcs, 8 * nf, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<size_t> ord(nf);
+    for (size_t i = 0; i < nf; i++) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+    u.fl_final_ids.resize(nf);
+    u.fl_final_costs.resize(nf);
+    for (size_t i = 0; i < nf; i++) {
+        u.fl_final_ids[i] = ids[ord[i]];
+        u.fl_final_costs[i] = fcv[ord[i]];
+    }
+    const uint64_t sk = (uint64_t)start_idx;
+    auto it = std::lower_bound(u.fl_nodes.begin(), u.fl_nodes.end(), sk);
+    if (start_idx < 0 || it == u.fl_nodes.end() || *it != sk) {
+        u.status = LB_DECODE_FAILURE;
+        u.msg = "surviving arcs do not connect to the start node";
+    } else {
+        u.fl_start = it - u.fl_nodes.begin();
+        if (nf == 0) {
+            u.status = LB_DECODE_FAILURE;
+            u.msg = "no terminal node survived pruning";
+        }
+    }
+    *out = res.release();
+    return LB_OK;
+}
+
 // prune_lattice (lattice.py:365-431) on the device for a host work lattice.
 int lb_prune_lattice(int32_t device, int32_t t, const int64_t *frame_off, const double *fwd, const int64_t *block_off,
                      const int32_t *from_idx, const int32_t *to_idx, const uint8_t *emitting, const double *graph_cost,

@@ -151,4 +151,21 @@ __global__ void fl_finals(const unsigned long long *nodes, int nn, int T, const 
     }
 }
 
+// final nodes for a host-given work lattice: last-frame nodes whose token has a
+// finite final cost (fc[idx], the reference's final_token_costs), or all of them
+// with cost 0 for a partial result (lattice.py:576-580)
+__global__ void fl_finals_given(const unsigned long long *nodes, int nn, int T, const double *fc, long long nfc,
+                                int partial, long long *ids, double *fcs, unsigned long long *count) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+        if ((int)(nodes[i] >> 32) != T) continue;
+        const long long idx = (long long)(unsigned)nodes[i];
+        const double c = partial ? 0.0 : (idx < nfc ? fc[idx] : __longlong_as_double(0x7FF0000000000000ll));
+        if (partial || c < __longlong_as_double(0x7FF0000000000000ll)) {
+            const unsigned long long k = atomicAdd(count, 1ull);
+            ids[k] = i;
+            fcs[k] = c;
+        }
+    }
+}
+
 }  // namespace lbk

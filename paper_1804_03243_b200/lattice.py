@@ -260,42 +260,47 @@ def prune_lattice(lat: WorkLattice, frontier: FrameTokens, lattice_beam: float,
     lat.node_extra = ne
 
 
-def finalize_lattice(lat: WorkLattice) -> FinalLattice:
+def finalize_lattice(lat: WorkLattice, device: int = 0) -> FinalLattice:
     """Compact surviving arcs, renumber nodes densely by (frame, idx), sort arcs
-    canonically by (from, to, ilabel, olabel, graph, acoustic) — lattice.py:537-598."""
+    canonically by (from, to, ilabel, olabel, graph, acoustic) -- lattice.py:537-598
+    of `latbeam` -- on the device (C-ABI lb_finalize_lattice: CUB radix sorts,
+    unique and the six stable LSD passes of np.lexsort, as the decode path's own
+    finaliser does, csrc/lb_lattice.cuh)."""
+    import ctypes as C
+
+    from . import _lib
+    from .errors import InternalInvariantError, UsageError
     t = lat.live_arc_table()
-    if len(t["slots"]) == 0:
-        raise DecodeFailure("no lattice arcs survived pruning")
-    fk = (t["from_frame"].astype(np.int64) << 32) | t["from_idx"].astype(np.int64)
-    tk = (t["to_frame"].astype(np.int64) << 32) | t["to_idx"].astype(np.int64)
-    keys = np.unique(np.concatenate([fk, tk]))
-    fid = np.searchsorted(keys, fk)
-    tid = np.searchsorted(keys, tk)
-    order = np.lexsort((t["acoustic_cost"], t["graph_cost"], t["olabel"], t["ilabel"], tid, fid))
-    nframe = keys >> 32
-    nidx = keys & 0xFFFFFFFF
-    sk = np.int64(lat.start_idx)
-    sp = int(np.searchsorted(keys, sk))
-    if sp >= len(keys) or keys[sp] != sk:
-        raise DecodeFailure("surviving arcs do not connect to the start node")
+    n = len(t["slots"])
+    fk = np.ascontiguousarray((t["from_frame"].astype(np.uint64) << np.uint64(32)) | t["from_idx"].astype(np.uint64))
+    tk = np.ascontiguousarray((t["to_frame"].astype(np.uint64) << np.uint64(32)) | t["to_idx"].astype(np.uint64))
+    il = np.ascontiguousarray(t["ilabel"], dtype=np.int32)
+    ol = np.ascontiguousarray(t["olabel"], dtype=np.int32)
+    g = np.ascontiguousarray(t["graph_cost"], dtype=np.float64)
+    ac = np.ascontiguousarray(t["acoustic_cost"], dtype=np.float64)
     last = lat.num_frames
-    at_last = nframe == last
-    if lat.partial:
-        fids = np.flatnonzero(at_last)
-        fcs = np.zeros(len(fids))
-    else:
-        tc = lat.final_token_costs
-        fin = at_last & np.isfinite(tc[np.where(at_last, nidx, 0)])
-        fids = np.flatnonzero(fin)
-        fcs = tc[nidx[fids]]
-    if len(fids) == 0:
-        raise DecodeFailure("no terminal node survived pruning")
-    return FinalLattice(len(keys), sp, fids.astype(np.int64), fcs.astype(np.float64),
-                        fid[order].astype(np.int64), tid[order].astype(np.int64),
-                        t["ilabel"][order].astype(np.int64), t["olabel"][order].astype(np.int64),
-                        t["graph_cost"][order].astype(np.float64),
-                        t["acoustic_cost"][order].astype(np.float64),
-                        nframe.astype(np.int64), nidx.astype(np.int64), last)
+    fc = None if lat.partial or lat.final_token_costs is None else \
+        np.ascontiguousarray(lat.final_token_costs, dtype=np.float64)
+    L = _lib.lib()
+    P32, PD, PU64 = _lib.P32, _lib.PD, _lib.PU64
+    res = _lib.PV()
+    rc = L.lb_finalize_lattice(int(device), n, fk.ctypes.data_as(PU64), tk.ctypes.data_as(PU64),
+                               il.ctypes.data_as(P32), ol.ctypes.data_as(P32), g.ctypes.data_as(PD),
+                               ac.ctypes.data_as(PD), int(lat.start_idx), int(last), int(bool(lat.partial)),
+                               0 if fc is None else len(fc), None if fc is None else fc.ctypes.data_as(PD),
+                               C.byref(res))
+    if rc != 0:
+        raise (UsageError if rc == 2 else InternalInvariantError)(_lib.last_error())
+    try:
+        st = C.c_int32()
+        msg = C.create_string_buffer(256)
+        L.lb_result_status(res, 0, C.byref(st), msg, 256, None, 0)
+        if st.value == 1:
+            raise DecodeFailure(msg.value.decode())
+        from .decoder import _final_lattice
+        return _final_lattice(res, 0, last)
+    finally:
+        L.lb_result_free(res)
 
 
 def write_lattice_text(fl: FinalLattice) -> str:

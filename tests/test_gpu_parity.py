@@ -653,3 +653,36 @@ def test_row_prefetch_and_its_fallbacks(oracle_mod, monkeypatch):
     monkeypatch.setenv("LB_NO_ROWPF", "1")
     outs, _ = decode_batch_resident(w, aligned, cfg)
     assert [x["total_cost"] for x in outs] == tc.tolist()
+
+
+def test_finalize_lattice_single_op():
+    """finalize_lattice (lattice.py:537-598) on the device for a work lattice:
+    equal to the decode's own device-finalised lattice, to the numpy restatement
+    (oracle/finalize_oracle.py) after a re-prune at a tighter beam, and the
+    reference's DecodeFailure when nothing survives."""
+    from oracle import finalize_oracle as FO
+    n = 0
+    for seed in range(16_000_000, 16_000_020):
+        w, m = synthetic.random_task(seed, allow_eps_cycles=seed % 2 == 0)
+        try:
+            r = lb.decode_utterance(w, m, lb.DecodeConfig(beam=9.0, lattice_beam=4.0, keep_work_lattice=True))
+        except lb.LatbeamError:
+            continue
+        lat = r.work_lattice
+        fl = lb.finalize_lattice(lat)
+        assert fl.same_lattice(r.lattice)
+        assert np.array_equal(fl.node_frame, r.lattice.node_frame) and np.array_equal(fl.node_idx, r.lattice.node_idx)
+        lb.prune_lattice(lat, lat.frames[-1], 1.0, final_costs=None if r.partial else lat.final_token_costs)
+        try:
+            want = FO.finalize(lat.live_arc_table(), lat.start_idx, lat.num_frames, lat.partial, lat.final_token_costs)
+        except ValueError as exc:
+            with pytest.raises(lb.DecodeFailure, match=str(exc)):
+                lb.finalize_lattice(lat)
+            continue
+        got = lb.finalize_lattice(lat)
+        assert got.num_nodes == want["num_nodes"] and got.start == want["start"]
+        for k in ("final_ids", "final_costs", "from_", "to", "ilabel", "olabel", "graph_cost", "acoustic_cost",
+                  "node_frame", "node_idx"):
+            assert np.array_equal(getattr(got, k), want[k]), k
+        n += 1
+    assert n >= 10
