@@ -486,9 +486,10 @@ def main(argv=None):
                "sample": f"{n} utterances x {frames or 'full-length'} frames of the job's list, "
                          f"oracle C port on {threads} threads ({cpu_model()})"}
 
-    ragged = None
+    ragged = auto_lanes = None
     if dist.rank == 0 and dist.world == 1 and not args.no_configs and not args.ragged:
         ragged = ragged_variant(args, dpool, step_resident, flush)
+        auto_lanes = auto_lanes_variant(resident, frames_mine, cfg, step_resident, flush)
 
     if dist.rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": dist.world,
@@ -498,7 +499,8 @@ def main(argv=None):
                        f"{min(args.pool, args.utts)} distinct matrices",
                "arcs_per_sec": arcs_all / (t_max / 1e3),
                "config": config_dict(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": launches, "clocks": ck, "ragged_variant": ragged, "configs_measured": configs}
+               "gpu_launches": launches, "clocks": ck, "ragged_variant": ragged,
+               "auto_lanes_variant": auto_lanes, "configs_measured": configs}
         print(json.dumps(out, default=_jsonable), flush=True)
     dist.close()
 
@@ -526,6 +528,29 @@ def phase_split(graph, resident, cfg, peak, step_resident, n_sub: int = 512) -> 
             "kernel_ms_profiled": tm["decode_ms"],
             "definition": "B_exp = 28 N + 16 N_scan + 8 N_cand summed over the utterances; emit time = "
                           "sum over lanes of their emit-phase time / lanes (LB_PHASE_PROFILE run)"}
+
+
+def auto_lanes_variant(resident, frames, cfg, step_resident, flush, steps: int = 2) -> dict:
+    """The same job with the library's default lane count (lanes=0: one 2-CTA lane
+    per SM pair, 74 on a B200) instead of the config's 64 -- not the headline,
+    which keeps BASELINE.json's 64 lanes."""
+    import dataclasses
+
+    import torch
+    c = dataclasses.replace(cfg, lanes=0)
+    step_resident(resident, c)
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step_resident(resident, c)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    return {"frames_per_s": frames * steps / (ms / 1e3), "lanes": "auto (one 2-CTA lane per SM pair)",
+            "steps": steps}
 
 
 def ragged_variant(args, dpool, step_resident, flush, steps: int = 2) -> dict:
