@@ -104,8 +104,10 @@ class Dist:
         if self.world > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            backend = "nccl" if backend_gpu else "gloo"
-            if backend_gpu:
+            # LB_BENCH_BACKEND=gloo: the timing reductions over gloo (e.g. two ranks
+            # sharing one GPU to exercise the multi-rank path; NCCL refuses that)
+            backend = os.environ.get("LB_BENCH_BACKEND") or ("nccl" if backend_gpu else "gloo")
+            if backend == "nccl":
                 import torch
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend)
@@ -371,7 +373,7 @@ def main(argv=None):
     from paper_1804_03243_b200 import synthetic
     from paper_1804_03243_b200.resident import decode_batch_resident
 
-    dev = dist.local
+    dev = dist.local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev)
     graph = synthetic.hclg_graph(0, num_states=args.states)
     cfg = lb.DecodeConfig(beam=13.0, max_active=7000, lanes=args.lanes, threads_per_lane=args.threads,
