@@ -270,7 +270,8 @@ def run_reference(args, dist: Dist):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "arcs_per_sec": total_a / total_t,
-           "config": config_dict(args, note="CPU sample of the same workload (same graph and utterances)"),
+           "config": config_dict(args),
+           "note": "CPU sample of the same workload (same graph, same 300-frame utterances of the job's list)",
            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
                             "sample": sample},
            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -292,6 +292,33 @@ def corpus_c1(n_utts=2):
     return cases
 
 
+def corpus_text():
+    """write_lattice_text (lattice.py:605-614) of the reference's own FinalLattice,
+    pinned by sha256 + length: random tasks and config C1's first utterance cut
+    to 40 frames (~50k-arc text)."""
+    import hashlib as _h
+    cases = []
+    for seed in range(3_000_000, 3_000_040):
+        w, m = RS.random_task(seed)
+        cfg = latbeam.DecodeConfig(beam=9.0, lattice_beam=4.0)
+        try:
+            res = latbeam.decode_utterance(w, m, cfg)
+        except latbeam.LatbeamError:
+            continue
+        txt = latbeam.write_lattice_text(res.lattice).encode()
+        cases.append(dict(kind="random", seed=seed, beam=9.0, lattice_beam=4.0, sha=_h.sha256(txt).hexdigest(),
+                          length=len(txt), graph_hash=graph_hash(w), matrix_hash=arr_hash(m.costs)))
+    w = RS.uniform_bench_graph(0, num_states=10_000, arcs_per_state=5, num_labels=500)
+    m = latbeam.CostMatrix(RS.bench_matrix(100, num_frames=300, num_labels=500).costs[:40].copy())
+    res = latbeam.decode_utterance(w, m, latbeam.DecodeConfig(beam=13.0, lattice_beam=8.0,
+                                                              max_lattice_arcs=20_000_000))
+    txt = latbeam.write_lattice_text(res.lattice).encode()
+    cases.append(dict(kind="c1_40", seed=0, beam=13.0, lattice_beam=8.0, sha=_h.sha256(txt).hexdigest(),
+                      length=len(txt), graph_hash=graph_hash(w), matrix_hash=arr_hash(m.costs)))
+    print(f"text corpus: {len(cases)} lattices, C1/40 text {len(txt)} bytes")
+    return cases
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["random", "max_active", "c1"]
     if "random" in which:
@@ -300,3 +327,5 @@ if __name__ == "__main__":
         save("max_active.npz", corpus_max_active())
     if "c1" in which:
         save("c1.npz", corpus_c1())
+    if "text" in which:
+        save("lattice_text.npz", corpus_text())

@@ -86,3 +86,17 @@ def test_random_task_golden_on_device(monkeypatch, mode):
         k = _check(c, got)
         kinds[k] = kinds.get(k, 0) + 1
     assert kinds.get("ok", 0) >= 60, kinds
+
+
+def test_lattice_text_golden_on_device():
+    """Device-decoded lattices written as text equal the reference's own text
+    (sha256), random tasks and a 40-frame C1 lattice."""
+    import hashlib
+
+    from test_oracle_golden import TEXT_CASES, _text_inputs
+    for c in TEXT_CASES:
+        w, m = _text_inputs(c)
+        r = lb.decode_utterance(w, m, lb.DecodeConfig(beam=float(c["beam"]), lattice_beam=float(c["lattice_beam"]),
+                                                      max_lattice_arcs=20_000_000))
+        txt = lb.write_lattice_text(r.lattice).encode()
+        assert len(txt) == int(c["length"]) and hashlib.sha256(txt).hexdigest() == str(c["sha"])

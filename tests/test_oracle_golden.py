@@ -172,3 +172,39 @@ def test_config1_full_utterance_golden(oracle_mod, utt):
     assert fl["num_nodes"] == int(c["fl_num_nodes"]) and len(fl["from_"]) == int(c["fl_num_arcs"])
     assert arr_hash(fl["from_"], fl["to"], fl["ilabel"], fl["olabel"], fl["graph_cost"],
                     fl["acoustic_cost"], fl["final_ids"], fl["final_costs"]) == str(c["fl_hash"])
+
+
+TEXT_CASES = load("lattice_text.npz")
+
+
+def _text_inputs(c):
+    if str(c["kind"]) == "random":
+        w, m = synthetic.random_task(int(c["seed"]))
+    else:
+        w = synthetic.config_graph("C1")
+        m = synthetic.CostMatrix(synthetic.config_matrix("C1", 0).costs[:40].copy())
+    assert graph_hash(w) == str(c["graph_hash"]) and arr_hash(m.costs) == str(c["matrix_hash"])
+    return w, m
+
+
+@pytest.mark.parametrize("idx", range(len(TEXT_CASES)))
+def test_lattice_text_golden(oracle_mod, idx):
+    """The reference's write_lattice_text of its own lattice (sha256 + length,
+    tests/golden/make_golden.py corpus_text) equals the native text writer
+    (lb_lattice_text, host-only) over the oracle's FinalLattice: pins the
+    finalised arrays and the Python-repr float formatting at once, up to a
+    ~140k-arc C1 lattice."""
+    import hashlib
+
+    import paper_1804_03243_b200 as lb
+    c = TEXT_CASES[idx]
+    w, m = _text_inputs(c)
+    ref = oracle_mod.decode(w, m, float(c["beam"]), lattice_beam=float(c["lattice_beam"]),
+                            max_lattice_arcs=20_000_000)
+    assert ref.ok
+    f = ref.final
+    fl = lb.FinalLattice(f["num_nodes"], f["start"], f["final_ids"], f["final_costs"], f["from_"], f["to"],
+                         f["ilabel"], f["olabel"], f["graph_cost"], f["acoustic_cost"])
+    txt = lb.write_lattice_text(fl).encode()
+    assert len(txt) == int(c["length"])
+    assert hashlib.sha256(txt).hexdigest() == str(c["sha"])
