@@ -1015,8 +1015,11 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     int lanes_guess = cfg->lanes > 0 ? cfg->lanes : std::min<int>(n, std::max(1, g->sms / 2));
     lanes_guess = std::max(1, std::min(lanes_guess, n > 0 ? n : 1));
     const int bpl = std::max(1, (g->sms * 4) / lanes_guess);   // batched: blocks per lane per phase kernel
+    // batched mode: every warp that gets tokens leaves at most one partly used
+    // chunk, and a wave's lane groups may run up to sms*4 blocks per lane (a group
+    // of one lane), so the tail is bounded by min(all warps, token groups) chunks
     const int64_t ccap = batched ? std::min<int64_t>(g->A_emit, max_tok * g->max_edeg) +
-                                       (int64_t)(bpl * BNW + 1) * BCCH
+                                       (std::min<int64_t>((int64_t)g->sms * 4 * BNW, (max_tok + 31) / 32) + 1) * BCCH
                                  : cand_capacity(g, max_tok, C, threads);
     // lanes: requested, else as many as fit a memory budget (<= 1 wave of SMs)
 

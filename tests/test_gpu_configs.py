@@ -158,3 +158,20 @@ def test_c4_ragged_refill_full_graph(oracle_mod):
     assert [r.total_cost for r in res] == tc.tolist()
     for r, c in zip(res, cnt):
         assert _counters(r) == [c[0], c[1], c[6]]
+
+
+@pytest.mark.parametrize("n,mode,want_lattice", [(44, None, True), (64, "batched", False)])
+def test_c1_large_batched_batches(oracle_mod, monkeypatch, n, mode, want_lattice):
+    """C1's dense 10k-state graph (~48k candidates per lane-frame, no max-active) in
+    the batched mode at 44 / 64 lanes: its candidate buffers hold every warp's
+    partly used chunk (a round-2 sweep found 44+ lanes overflowing them)."""
+    if mode:
+        monkeypatch.setenv("LB_MODE", mode)
+    w = graph("C1")
+    d = synthetic.CONFIGS["C1"]["decode"]
+    mats = [np.ascontiguousarray(synthetic.config_matrix("C1", u % 20, num_frames=60).costs) for u in range(n)]
+    res = lb.decode_batch(w, mats, lb.DecodeConfig(beam=d["beam"], lattice_beam=d["lattice_beam"],
+                                                   max_lattice_arcs=20_000_000), want_lattice=want_lattice)
+    tc, st, _ = oracle_mod.decode_batch_mt(w, mats, d["beam"])
+    assert all(st == 0)
+    assert [r.total_cost for r in res] == tc.tolist()

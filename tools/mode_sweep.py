@@ -28,6 +28,7 @@ modes = [("auto", None, 0), ("batched", "batched", 0), ("lane2", "lane", 2), ("l
 for U in Us:
     tens = [pool[u % 16] for u in range(U)]
     row = []
+    ref = None
     for label, mode, ctas in modes:
         if mode:
             os.environ["LB_MODE"] = mode
@@ -35,9 +36,15 @@ for U in Us:
             os.environ.pop("LB_MODE", None)
         cfg = lb.DecodeConfig(beam=d["beam"], max_active=d["max_active"], ctas_per_lane=ctas)
         try:
-            decode_batch_resident(g, tens, cfg)
+            outs, _ = decode_batch_resident(g, tens, cfg)
+            bad = [o["status"] for o in outs if o["status"] != 0]
+            if bad:
+                row.append(f"{label}=status{bad[0]}")
+                continue
+            costs = [o["total_cost"] for o in outs]
+            ref = ref if label != "auto" else costs
             ms = min(decode_batch_resident(g, tens, cfg)[1]["decode_ms"] for _ in range(2))
-            row.append(f"{label}={U * T / ms * 1e3 / 1e3:.1f}k")
+            row.append(f"{label}={U * T / ms * 1e3 / 1e3:.1f}k" + ("" if costs == ref else "(MISMATCH)"))
         except Exception as exc:   # noqa: BLE001 - e.g. clusters that cannot be co-resident
             row.append(f"{label}=err({type(exc).__name__})")
     print(f"{name} U={U}: " + " ".join(row), flush=True)
