@@ -933,8 +933,14 @@ void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched,
     // at C=4; 44: 415k vs 349k batched and 350k at C=2 with C=3; measured with
     // tools/mode_auto.sh).  1-4 utterances stay batched; lattice decodes keep the
     // batched / 2-CTA rule.
-    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= 5) {
-        const size_t dsm = lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX);
+    // Heavy frames (max-active >= 10k, or no cap on a >= 1M-state graph) already
+    // favour 8-CTA lanes from 2 utterances (C5 shape, tools/mode_sweep.py: 2 utts
+    // 16.9k vs 15.3k frames/s batched, 4 utts 32.7k vs 24.0k); lighter ones stay
+    // batched up to 4 (C2: 34.5k vs 33.6k at 2; C1: 75.9k vs 64.5k at 2).
+    const bool heavy = cfg->max_active >= 10000 || (cfg->max_active == 0 && g->S >= 1000000);
+    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= (heavy ? 2 : 5)) {
+        const bool acs = (size_t)D * 8 <= ACROW_SMEM_MAX;
+        const size_t dsm = lane_dyn_smem(threads, D, acs, acs && D % 2 == 0);   // with the row prefetch buffers
         for (int c : {8, 4, 3}) {
             if (n <= max_coresident_clusters(g, c, threads, dsm)) {
                 batched = false;
@@ -945,7 +951,8 @@ void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched,
     }
     C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
     if (getenv("LB_MODE_DEBUG"))
-        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d)\n", n, batched ? "batched" : "lane", C,
+        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d, smem without row prefetch)\n", n,
+                batched ? "batched" : "lane", C,
                 max_coresident_clusters(g, 3, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
                 max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
                 max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
