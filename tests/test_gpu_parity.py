@@ -686,3 +686,49 @@ def test_finalize_lattice_single_op():
             assert np.array_equal(getattr(got, k), want[k]), k
         n += 1
     assert n >= 10
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_compute_sanitizer_round2_paths(tool):
+    """compute-sanitizer on the round-2 paths: refilling lanes fed through the
+    streamed ring with slot reuse (8 jobs, 2 lanes, 3 slots) and the row prefetch,
+    mixed-width launches, HBM-resident f32 rows, two replicas on one device, and
+    the prune_lattice / finalize_lattice single ops."""
+    import os
+    import shutil
+    import subprocess
+    import sys
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = (
+        "import sys, os; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch\n"
+        "import paper_1804_03243_b200 as lb\n"
+        "from paper_1804_03243_b200 import synthetic\n"
+        "from paper_1804_03243_b200.resident import decode_batch_resident\n"
+        "w = synthetic.hclg_graph(5, num_states=20000, pool_size=500, num_pdfs=100)\n"
+        "ms = [np.ascontiguousarray(synthetic.hclg_matrix(40 + i, num_frames=4 + i, num_pdfs=100).costs) for i in range(8)]\n"
+        "os.environ['LB_RING_SLOTS'] = '3'\n"
+        "a = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300, lanes=2), want_lattice=False)\n"
+        "os.environ['LB_MIXED_N3'] = '1'\n"
+        "b = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300, lanes=2), want_lattice=False)\n"
+        "del os.environ['LB_MIXED_N3']\n"
+        "f = decode_batch_resident(w, [torch.from_numpy(m.astype(np.float32)).cuda() for m in ms],\n"
+        "                          lb.DecodeConfig(beam=10.0, max_active=300, lanes=2))[0]\n"
+        "c = lb.decode_batch(w, ms[:4], lb.DecodeConfig(beam=10.0, max_active=300, devices=(0, 0)), want_lattice=False)\n"
+        "assert [x.total_cost for x in a] == [x.total_cost for x in b]\n"
+        "assert [x.total_cost for x in a[:4]] == [x.total_cost for x in c]\n"
+        "assert all(o['status'] == 0 for o in f)\n"
+        "t, m = synthetic.random_task(21, allow_eps_cycles=True)\n"
+        "r = lb.decode_utterance(t, m, lb.DecodeConfig(beam=9.0, lattice_beam=4.0, keep_work_lattice=True))\n"
+        "lat = r.work_lattice\n"
+        "assert lb.finalize_lattice(lat).same_lattice(r.lattice)\n"
+        "lb.prune_lattice(lat, lat.frames[-1], 1.0, final_costs=None if r.partial else lat.final_token_costs)\n"
+        "print('ok', [x.total_cost for x in a])\n" % root)
+    res = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable, "-c", prog],
+                         capture_output=True, text=True, timeout=1500)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-6000:]
+    assert "ok" in res.stdout and "ERROR SUMMARY: 0 errors" in out, out[-3000:]
