@@ -1040,7 +1040,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     int n3 = 0;
     if (refill_mode && C == 2 && cfg->ctas_per_lane == 0 && n > lanes && !getenv("LB_NO_MIXED"))
         n3 = std::max(0, std::min(lanes, g->sms - 2 * lanes));
-    if (const char *e = getenv("LB_MIXED_N3")) n3 = std::max(0, std::min(lanes, atoi(e)));
+    if (const char *e = getenv("LB_MIXED_N3"))   // test knob: force n3 (2-CTA refilling lanes only)
+        if (refill_mode && C == 2 && n > lanes) n3 = std::max(0, std::min(lanes, atoi(e)));
     const int Ca = n3 > 0 ? 3 : C;   // CTA segments allocated per lane
     if (getenv("LB_MODE_DEBUG")) fprintf(stderr, "[lanes] %d lanes, %d of them 3-CTA, C=%d\n", lanes, n3, C);
     const size_t per_lane = lane_bytes(S, Ca, ccap, tok_cap, lat_cap, path_cap, tmax, packs, lat, batched);

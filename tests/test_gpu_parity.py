@@ -711,10 +711,11 @@ def test_compute_sanitizer_round2_paths(tool):
         "w = synthetic.hclg_graph(5, num_states=20000, pool_size=500, num_pdfs=100)\n"
         "ms = [np.ascontiguousarray(synthetic.hclg_matrix(40 + i, num_frames=4 + i, num_pdfs=100).costs) for i in range(8)]\n"
         "os.environ['LB_RING_SLOTS'] = '3'\n"
+        "os.environ['LB_MODE'] = 'lane'\n"
         "a = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300, lanes=2), want_lattice=False)\n"
         "os.environ['LB_MIXED_N3'] = '1'\n"
         "b = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, max_active=300, lanes=2), want_lattice=False)\n"
-        "del os.environ['LB_MIXED_N3']\n"
+        "del os.environ['LB_MIXED_N3']; del os.environ['LB_MODE']\n"
         "f = decode_batch_resident(w, [torch.from_numpy(m.astype(np.float32)).cuda() for m in ms],\n"
         "                          lb.DecodeConfig(beam=10.0, max_active=300, lanes=2))[0]\n"
         "c = lb.decode_batch(w, ms[:4], lb.DecodeConfig(beam=10.0, max_active=300, devices=(0, 0)), want_lattice=False)\n"
