@@ -1079,8 +1079,6 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     const size_t acrow_bytes = (size_t)D * 8;
     p.acrow_smem = acrow_bytes <= ACROW_SMEM_MAX;
     p.prof = nullptr;
-    const char *ex = getenv("LB_EXP");
-    p.exp = ex ? atoi(ex) : 0;
     p.ready = d_ready;
     if (batched && d_ready) return set_err(LB_INTERNAL, "progressive staging needs the lane kernel");
     p.costs_f32 = costs_f32;
@@ -2600,7 +2598,6 @@ static int expand_common(lb_graph *g, const int32_t *states, const double *costs
     p.max_tokens = 1ll << 40;
     p.D = D;
     p.acrow_smem = 0;
-    p.exp = 0;
     p.ready = nullptr;
     const int esm = (int)lane_dyn_smem(768, 1, false);
     CK(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, esm));

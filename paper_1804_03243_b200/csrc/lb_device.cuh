@@ -292,7 +292,6 @@ struct Params {
     int collect_packs;
     int acrow_smem;
     unsigned long long *prof;   // optional per-phase ns accumulators (LB_PHASE_PROFILE=1)
-    int exp;                    // timing experiments (LB_EXP, profiling only; results not exact)
     int costs_f32;              // job cost matrices are f32 (widened exactly to f64 at the row load)
     int row_pf;                 // two row buffers: the next frame's row is prefetched (Lane::row_async)
     int _pad3;

@@ -255,11 +255,6 @@ struct Lane {
 #else
     static constexpr int WUNR = 1;   // candidates per thread per winners batch (next batch prefetched)
 #endif
-#ifdef LB_AUNR
-    static constexpr int AUNR = LB_AUNR;
-#else
-    static constexpr int AUNR = 1;   // touched states per thread per aggregate batch (2 spills at 80 regs)
-#endif
 #ifdef LB_EUNR
     static constexpr int EUNR = LB_EUNR;
 #else
