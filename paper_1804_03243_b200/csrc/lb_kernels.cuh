@@ -597,7 +597,7 @@ struct Lane {
         const double inv_w = __drcp_rn(width);
         const int4 *cb = L.cand + (size_t)G.rank * L.ccap;
         const int *cbi = L.candi + (size_t)G.rank * L.ccap;
-        const unsigned long long *pk = L.pk;
+        unsigned long long *pk = L.pk;
         unsigned *f0 = front(0);
         int *ntouched = &lane_sm.ntouched[par], *nf0 = &lane_sm.nfr[0];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -655,8 +655,20 @@ struct Lane {
                 const unsigned v = (unsigned)e[u].x & ~EPS_FLAG;
                 const double cand = __hiloint2double(e[u].w, e[u].z);
                 const bool own = e[u].x != -1 && pw[u] == pack_word(cand, (unsigned)e[u].y);
-                const unsigned mo = __ballot_sync(FULL, own);
-                if (own) {
+                const bool seed = own && cand <= cutoff;
+#ifndef LB_WIN_KEEP_ALL
+                // An owner above the cutoff can only be kept if an epsilon offer
+                // (<= cutoff) improves it later, and such an offer finds the word
+                // reset and lists the state as epsilon-reached (erec).  So it is
+                // reset here and never enters the winner list: aggregate touches
+                // only the seeds (about half the owners at max-active).
+                if (own && !seed) rst_u64(pk + v, SENT);
+                const bool listed = seed;
+#else
+                const bool listed = own;
+#endif
+                const unsigned mo = __ballot_sync(FULL, listed);
+                if (listed) {
                     const int j = sw.n + __popc(mo & lt);
                     sw.v[j] = v;
                     sw.a[j] = (unsigned)e[u].y;
@@ -664,7 +676,6 @@ struct Lane {
                     sw.c[j] = cand;
                 }
                 sw.n += __popc(mo);
-                const bool seed = own && cand <= cutoff;
                 nseed += seed;
                 // only states with epsilon arcs enter the closure
                 const bool fz = seed && ((unsigned)e[u].x & EPS_FLAG);
