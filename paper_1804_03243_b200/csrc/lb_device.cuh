@@ -294,7 +294,7 @@ struct Params {
     unsigned long long *prof;   // optional per-phase ns accumulators (LB_PHASE_PROFILE=1)
     int costs_f32;              // job cost matrices are f32 (widened exactly to f64 at the row load)
     int row_pf;                 // two row buffers: the next frame's row is prefetched (Lane::row_async)
-    int efilter;                // emit's per-CTA duplicate filter (Lane::emit)
+    int _pad3;
     const int *ready;           // progressive host staging (mapped): rows of frames < *ready are
                                 // in place for every utterance; nullptr = all rows ready
     // Streaming host staging for refilling lanes (mapped pinned ring of

@@ -227,12 +227,9 @@ constexpr int SWW = 96;   // winners stages: touched {v, arc, pred, cost} and ro
 constexpr int WSCR = (SWT * 32 + SW * 4) > SWW * 32 ? (SWT * 32 + SW * 4) : SWW * 32;
 static_assert(SWW * 20 + SWW * 12 <= WSCR, "winners stages fit the warp scratch");
 // `row_pf`: two row buffers (the next frame's row is prefetched, Lane::row_async).
-// `efilter`: the emit duplicate filter's table (Lane::emit, EFT entries of 8 bytes).
-constexpr int EFT = 2048;
-inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem, bool row_pf = false, bool efilter = false) {
+inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem, bool row_pf = false) {
     const size_t nw = (size_t)threads / 32;
-    return (acrow_smem ? (size_t)D * 8 * (row_pf ? 2 : 1) : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4 +
-           (efilter ? (size_t)EFT * 8 : 0);
+    return (acrow_smem ? (size_t)D * 8 * (row_pf ? 2 : 1) : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
 }
 constexpr int CAND_CHUNK = 256;   // Lane::CCH
 
@@ -287,15 +284,6 @@ struct Lane {
         return reinterpret_cast<int *>(scratch_all() + (blockDim.x >> 5) * WSCR);
     }
     __device__ __forceinline__ char *scratch() const { return scratch_all() + (threadIdx.x >> 5) * WSCR; }
-    // emit duplicate filter: per CTA, (f32 key << 32) | state of the best candidate
-    // this CTA has sent to a state (direct-mapped, lossy; SENT = empty)
-    __device__ __forceinline__ unsigned long long *eftab() const {
-        return reinterpret_cast<unsigned long long *>(whist_all() + (blockDim.x >> 5) * NBINS);
-    }
-    __device__ __forceinline__ void eftab_clear() const {
-        if (p.efilter)
-            for (int i = threadIdx.x; i < EFT; i += blockDim.x) eftab()[i] = SENT;
-    }
     // u32 stage q (0, 1) of this warp's scratch (winners)
     __device__ __forceinline__ WStage stage(int q) const {
         WStage st;
@@ -481,20 +469,6 @@ struct Lane {
                 if (cand[u] < inf_d()) {
                     const unsigned long long word = pack_word(cand[u], aa[u]);
                     em[u] = (unsigned)(word >> 32) <= bound_key;
-                    if (em[u] && p.efilter) {
-                        // This CTA already sent this state a strictly smaller key
-                        // (its RED completes before the emit barrier), so this
-                        // candidate can be neither the state's winner nor the frame
-                        // best: no RED, no candidate record.  Equal keys are kept
-                        // (the arc id breaks the tie).  Races on the table only make
-                        // it forget entries.
-                        const unsigned key = (unsigned)(word >> 32);
-                        unsigned long long *slot = eftab() + ((r[u].x * 0x9E3779B1u) >> (32 - 11));
-                        const unsigned long long ent = *slot;
-                        if ((unsigned)ent == (unsigned)r[u].x && (unsigned)(ent >> 32) < key) em[u] = false;
-                        else if ((unsigned)ent != (unsigned)r[u].x || key < (unsigned)(ent >> 32))
-                            *slot = ((unsigned long long)key << 32) | (unsigned)r[u].x;
-                    }
                     if (em[u]) red_min_u64(pk + r[u].x, word);
                 }
                 const unsigned bb = __ballot_sync(FULL, em[u]);
@@ -1241,7 +1215,6 @@ __device__ __forceinline__ void decode_one(const GraphDev &g, const Params &p, c
                         t - 1);
         }
         if (g.has_eps) ln.fix_preds((t - 1) & 1, t - 1, tbp, np);
-        ln.eftab_clear();
         __syncthreads();
         const double best = ln.emit(io.tok_state + tbp, io.tok_cost + tbp, np, beam_eff, t);
         ln.clear_next_counters();   // frame t-1's readers are past the emit barrier
