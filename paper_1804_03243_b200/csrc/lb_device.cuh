@@ -382,6 +382,22 @@ __device__ __forceinline__ void epswin_min(EpsWin *p, unsigned long long word, d
     }
 }
 
+// The same, also telling whether this offer was the round's FIRST improving one
+// for the state (its CAS replaced the idle value): the caller then lists the
+// state in the next frontier, exactly once per round.
+__device__ __forceinline__ bool epswin_min_first(EpsWin *p, unsigned long long word, double cost) {
+    ulonglong2 cur = make_ulonglong2(~0ull, ~0ull);
+    const ulonglong2 val = make_ulonglong2(word, (unsigned long long)__double_as_longlong(cost));
+    bool first = true;
+    for (;;) {
+        const ulonglong2 prev = cas128(p, cur, val);
+        if (prev.x == cur.x && prev.y == cur.y) return first;
+        if (prev.x <= word) return false;
+        cur = prev;
+        first = false;
+    }
+}
+
 // Global-space atomics with their results (explicit .global: a generic 64-bit
 // atomicMin would carry a shared-memory CAS fallback path).
 __device__ __forceinline__ unsigned long long atom_min_u64(unsigned long long *a, unsigned long long v) {
