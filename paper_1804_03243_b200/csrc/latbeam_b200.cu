@@ -151,7 +151,6 @@ struct Workspace {
     ERec *erec = nullptr;
     double *msnap = nullptr, *tcost = nullptr, *f0cost = nullptr;
     unsigned *tarc = nullptr, *etouched = nullptr;
-    uint2 *frng = nullptr;
     EpsWin *rpk = nullptr;
     unsigned *tag = nullptr, *touched = nullptr, *fr = nullptr, *fix = nullptr, *round_ctr = nullptr;
     int4 *cand = nullptr;
@@ -194,7 +193,7 @@ size_t lane_bytes(int64_t S, int C, int64_t ccap, int64_t tok_cap, int64_t lat_c
                   bool packs, bool lat, bool batched) {
     // per state: rpk 32 + tag 4 + fr/fix (12 per CTA), then the mode's own layout
     const size_t per_state = batched ? 32 + 32 + 4 + (size_t)C * 16
-                                     : 8 + 4 + 16 + 8 + 32 + 4 + (size_t)C * 32;   // pk tokidx erec msnap rpk tag
+                                     : 8 + 4 + 16 + 8 + 32 + 4 + (size_t)C * 16;   // pk tokidx erec msnap rpk tag
     const size_t per_cand = batched ? 20 + 4 : 20 + 4 + 8 + 4 + 4 + 8 + 4;       // + winner payload, f0cost
     return (size_t)S * per_state + (size_t)C * ccap * per_cand +
            (size_t)tok_cap * (20 + (packs ? 8 : 0) + (lat ? 16 : 0)) + (size_t)lat_cap * 28 + (size_t)path_cap * 4 +
@@ -303,7 +302,6 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
         CK(A(&w.tarc, nc * cc * nl));
         CK(A(&w.f0cost, nc * cc * nl));
         CK(A(&w.etouched, nc * S * nl));
-        CK(A(&w.frng, 2 * nc * S * nl));
     }
     CK(A(&w.rpk, 2 * S * nl));
     CK(A(&w.tag, S * nl));
@@ -362,7 +360,6 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
             x.tarc = w.tarc + l * nc * cc;
             x.f0cost = w.f0cost + l * nc * cc;
             x.etouched = w.etouched + l * nc * S;
-            x.frng = w.frng + l * 2 * nc * S;
         }
         x.rpk = w.rpk + l * 2 * S;
         x.tag = w.tag + l * S;

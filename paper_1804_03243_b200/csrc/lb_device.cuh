@@ -245,7 +245,6 @@ struct LaneWs {
     unsigned *tarc;            // [C][ccap] winner arc
     double *f0cost;            // [C][ccap] round-0 epsilon frontier costs (seeds)
     unsigned *etouched;        // [C][S] states first reached by an epsilon offer this frame
-    uint2 *frng;               // [2][C][S] epsilon out-arc range of each frontier entry (rounds >= 1)
 };
 
 // One utterance slot of a wave.

@@ -314,10 +314,7 @@ struct Lane {
         return L.fr + ((size_t)(r & 1) * L.C + G.rank) * L.S;
     }
     __device__ __forceinline__ EpsWin *rpk(int r) const { return L.rpk + (size_t)(r & 1) * L.S; }
-    // out-arc ranges carried with the frontier entries of rounds >= 1
-    __device__ __forceinline__ uint2 *frange(int r) const {
-        return L.frng + ((size_t)(r & 1) * L.C + G.rank) * L.S;
-    }
+
     __device__ __forceinline__ unsigned *fixes() const { return L.fix + (size_t)G.rank * L.S; }
     __device__ __forceinline__ int *wmap() const { return own_all() + (threadIdx.x >> 5) * WMAP; }
 
@@ -838,8 +835,7 @@ struct Lane {
             const int nf = lane_sm.nfr[r % 3];
             const unsigned *fs = front(r);
             unsigned *fsn = front(r + 1);
-            const uint2 *frs = frange(r);
-            uint2 *frsn = frange(r + 1);
+
             int *nnext = &lane_sm.nfr[(r + 1) % 3];
             if (threadIdx.x == 0) lane_sm.nfr[(r + 2) % 3] = 0;   // read at round r-1's start, one barrier ago
             EpsWin *rprev = rpk(r + 1);                         // == rpk(r - 1)
@@ -859,9 +855,7 @@ struct Lane {
 #pragma unroll
                 for (int u = 0; u < EUNR; u++) {
                     if (v[u] == 0xFFFFFFFFu) continue;
-                    // rounds >= 1: the range came with the frontier entry (its load
-                    // overlapped the previous round's offer)
-                    er[u] = r > 0 ? __ldcg(frs + k0 + u * bd) : gld2(g.erng + v[u]);
+                    er[u] = gld2(g.erng + v[u]);
                     if (r > 0) {
                         const ulonglong2 w2 = rld_u128(rprev + v[u]);
                         rst_u128(rprev + v[u], make_ulonglong2(~0ull, ~0ull));
@@ -888,7 +882,6 @@ struct Lane {
                         c_ecand++;
                         const unsigned x = (unsigned)rr.x;
                         const unsigned long long word = pack_word(cand, (unsigned)rr.y);
-                        const uint2 xr = gld2(g.erng + x);   // x's range, in case x joins the next frontier
                         const unsigned long long old = atom_min_u64(pk + x, word);
                         if (old == SENT) {   // first reached by epsilon this frame
                             const int sl = agg_append(netouched);
@@ -908,7 +901,6 @@ struct Lane {
                             if (first) {
                                 const int sl = agg_append(nnext);
                                 __stcg(fsn + sl, x);
-                                __stcg(frsn + sl, xr);
                             }
                         }
                     }
