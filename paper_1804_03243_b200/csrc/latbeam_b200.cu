@@ -545,7 +545,7 @@ int validate_cfg(const lb_config *c) {
     if (c->threads_per_lane != 0 && c->threads_per_lane != 512 && c->threads_per_lane != LB_LANE_NT &&
         c->threads_per_lane != 768)
         return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
-    if (c->ctas_per_lane < 0 || c->ctas_per_lane > 8) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 8]");
+    if (c->ctas_per_lane < 0 || c->ctas_per_lane > 16) return set_err(LB_USAGE, "ctas_per_lane must be in [0, 16]");
     return LB_OK;
 }
 
@@ -931,17 +931,20 @@ void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched,
     // of which n are co-resident beats both the batched mode and 2-CTA lanes
     // (C2 graph, frames/s: 8 utts 124k vs 112k batched at C=8; 32: 373k vs 317k
     // at C=4; 44: 415k vs 349k batched and 350k at C=2 with C=3; measured with
-    // tools/mode_auto.sh).  1-4 utterances stay batched; lattice decodes keep the
-    // batched / 2-CTA rule.
-    // Heavy frames (max-active >= 10k, or no cap on a >= 1M-state graph) already
-    // favour 8-CTA lanes from 2 utterances (C5 shape, tools/mode_sweep.py: 2 utts
-    // 16.9k vs 15.3k frames/s batched, 4 utts 32.7k vs 24.0k); lighter ones stay
-    // batched up to 4 (C2: 34.5k vs 33.6k at 2; C1: 75.9k vs 64.5k at 2).
-    const bool heavy = cfg->max_active >= 10000 || (cfg->max_active == 0 && g->S >= 1000000);
-    if (!mode_env && cfg->ctas_per_lane == 0 && !lat && n >= (heavy ? 2 : 5)) {
+    // tools/mode_auto.sh).
+    // 16-CTA lanes (non-portable cluster size; 7 co-resident) took over the
+    // smallest batches, single utterances included, on every graph shape
+    // (tools/mode_sweep.py, frames/s): C5 1 utt 12.0k vs 8.1k batched, 6 utts
+    // 64.5k vs 50.9k at C=8; C1 1 utt 47.0k vs 36.4k batched, 4 utts 183k vs
+    // 133k at C=8; C2 1 utt 18.8k vs 17.6k batched, 4 utts 72.9k vs 68.4k.
+    // Lattice decodes take 16-CTA lanes only (C3 1 utt 14.5k vs 12.2k batched,
+    // 4 utts 56.2k vs 42.5k; C1 4 utts 133.6k vs 90.6k, where 8-CTA lanes lose
+    // to the batched mode) and otherwise stay batched / 2-CTA.
+    if (!mode_env && cfg->ctas_per_lane == 0 && n >= 1) {
         const bool acs = (size_t)D * 8 <= ACROW_SMEM_MAX;
         const size_t dsm = lane_dyn_smem(threads, D, acs, acs && D % 2 == 0);   // with the row prefetch buffers
-        for (int c : {8, 4, 3}) {
+        for (int c : {16, 8, 4, 3}) {
+            if (c == 16 ? getenv("LB_NO_C16") != nullptr : lat) continue;
             if (n <= max_coresident_clusters(g, c, threads, dsm)) {
                 batched = false;
                 autoC = c;
@@ -951,11 +954,12 @@ void choose_mode(lb_graph *g, int n, int D, const lb_config *cfg, bool &batched,
     }
     C = batched ? 1 : (cfg->ctas_per_lane > 0 ? cfg->ctas_per_lane : autoC);
     if (getenv("LB_MODE_DEBUG"))
-        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d, smem without row prefetch)\n", n,
+        fprintf(stderr, "[mode] n=%d %s C=%d (fit C3=%d C4=%d C8=%d C16=%d, smem without row prefetch)\n", n,
                 batched ? "batched" : "lane", C,
                 max_coresident_clusters(g, 3, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
                 max_coresident_clusters(g, 4, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
-                max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
+                max_coresident_clusters(g, 8, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)),
+                max_coresident_clusters(g, 16, threads, lane_dyn_smem(threads, D, (size_t)D * 8 <= ACROW_SMEM_MAX)));
 }
 
 // Streaming host ring of a refilling decode (lb_decode_batch, large 1-best batches).
@@ -1118,6 +1122,7 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     else return set_err(LB_USAGE, "threads_per_lane must be 512, 640 or 768");
 #undef LB_PICK
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    if (C > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));   // up to 16 on B200
     const GraphDev gd = g->dev();
 
     // Per-utterance output slots (status, costs, counters, best path) for the
@@ -1655,11 +1660,16 @@ int lb_decode_batch(const lb_graph *gc, int32_t n, const double *const *costs, c
     int lane_c = 1;
     choose_mode(g, n, D, cfg, batched_mode, lane_c);
     const bool lane_mode = !batched_mode;
-    const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
-                           !getenv("LB_E2E_COPY");
+    // Small batches (a few wide lanes) copy to HBM instead: a lane reading its
+    // rows over PCIe without the row prefetch stalls on every frame (one C2
+    // utterance on a 16-CTA lane: 19.3 ms zero-copy vs 16.6 ms with the copy;
+    // C5 28.3 vs 26.1 ms; tools/c2_timing.py).
     // Batches larger than one set of lanes refill lanes from the job queue; their
     // rows stream through a bounded pinned ring instead of a whole-batch stage.
     const int lanes_est = cfg->lanes > 0 ? cfg->lanes : std::max(1, g->sms / std::max(lane_c, 1));
+    const char *zc_min = getenv("LB_ZC_MIN");
+    const bool zero_copy = lane_mode && !cfg->want_lattice && (size_t)D * 8 <= ACROW_SMEM_MAX &&
+                           (n >= (zc_min ? atoi(zc_min) : 16) || n > lanes_est) && !getenv("LB_E2E_COPY");
     if (zero_copy && n > lanes_est && !cfg->collect_frame_packs && !getenv("LB_NO_RING") &&
         !getenv("LB_NO_REFILL")) {
         rc = decode_ring(g, n, costs, T, D, cfg, lanes_est, res.get());

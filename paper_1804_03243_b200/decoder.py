@@ -96,8 +96,8 @@ class DecodeConfig:
             raise UsageError("devices must be CUDA ordinals >= 0")
         if int(self.threads_per_lane) not in (0, 512, 640, 768):
             raise UsageError("threads_per_lane must be 512, 640 or 768")
-        if not 0 <= int(self.ctas_per_lane) <= 8:
-            raise UsageError("ctas_per_lane must be in [0, 8]")
+        if not 0 <= int(self.ctas_per_lane) <= 16:
+            raise UsageError("ctas_per_lane must be in [0, 16]")
 
     def to_c(self, want_lattice: bool, collect_frame_packs: bool) -> LbConfig:
         return LbConfig(float(self.beam), float(self.lattice_beam), float(self.acoustic_scale),

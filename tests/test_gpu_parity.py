@@ -261,6 +261,7 @@ def test_device_resident_and_zero_copy_paths_agree(oracle_mod, monkeypatch):
     cfg = lb.DecodeConfig(beam=12.0, max_active=1500)
     tc, st, _ = oracle_mod.decode_batch_mt(w, mats, 12.0, max_active=1500)
     assert all(st == 0)
+    monkeypatch.setenv("LB_ZC_MIN", "1")   # zero-copy even for a batch this small
     zc = lb.decode_batch(w, mats, cfg, want_lattice=False)
     monkeypatch.setenv("LB_E2E_COPY", "1")
     cp = lb.decode_batch(w, mats, cfg, want_lattice=False)
@@ -320,6 +321,7 @@ def test_progressive_zero_copy_staging(oracle_mod, monkeypatch, D):
     lengths, multi-threaded staging (> 8 MB), and the non-progressive path all
     equal the oracle bit-exactly."""
     monkeypatch.setenv("LB_MODE", "lane")
+    monkeypatch.setenv("LB_ZC_MIN", "1")
     w = synthetic.hclg_graph(8, num_states=200_000, pool_size=3000, num_pdfs=D)
     cfg = lb.DecodeConfig(beam=12.0, max_active=1500)
     for rnd in range(5):
@@ -361,7 +363,7 @@ def test_compute_sanitizer_clean(tool):
     """compute-sanitizer finds no memory error, shared-memory race or barrier misuse
     in small 1-best + lattice decodes with epsilon arcs and max-active:
     the batched mode and, except under racecheck (over 20 minutes on the lane
-    kernels' shared memory), 8-CTA lanes reading progressively staged host rows and
+    kernels' shared memory), 16-CTA lanes reading progressively staged host rows and
     2-CTA lanes with lattices."""
     import os
     import shutil
@@ -375,6 +377,7 @@ def test_compute_sanitizer_clean(tool):
         "import sys; sys.path.insert(0, %r)\n"
         "import paper_1804_03243_b200 as lb\n"
         "from paper_1804_03243_b200 import synthetic\n"
+        "import os; os.environ['LB_MODE'] = 'batched'\n"
         "w = synthetic.hclg_graph(5, num_states=20000, pool_size=500, num_pdfs=100)\n"
         "ms = [synthetic.hclg_matrix(9 + i, num_frames=6, num_pdfs=100) for i in range(2)]\n"
         "r = lb.decode_batch(w, ms, lb.DecodeConfig(beam=10.0, lattice_beam=3.0, max_active=300))\n"
@@ -382,8 +385,9 @@ def test_compute_sanitizer_clean(tool):
         "assert [x.total_cost for x in r] == [x.total_cost for x in q]\n"
         "if %r:\n"
         "    m6 = [synthetic.hclg_matrix(30 + i, num_frames=5, num_pdfs=100) for i in range(6)]\n"
+        "    del os.environ['LB_MODE']; os.environ['LB_ZC_MIN'] = '1'\n"
         "    q6 = lb.decode_batch(w, m6, lb.DecodeConfig(beam=10.0, max_active=300), want_lattice=False)\n"
-        "    import os; os.environ['LB_MODE'] = 'lane'\n"
+        "    os.environ['LB_MODE'] = 'lane'\n"
         "    l6 = lb.decode_batch(w, m6, lb.DecodeConfig(beam=10.0, lattice_beam=3.0, max_active=300))\n"
         "    assert [x.total_cost for x in q6] == [x.total_cost for x in l6]\n"
         "print('ok', [x.total_cost for x in r])\n" % (root, tool != "racecheck"))

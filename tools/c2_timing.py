@@ -1,4 +1,5 @@
-"""Single-utterance public-API timing (C2 / C5 graphs): wall vs library decode / h2d, per mode."""
+"""Single-utterance public-API timing (C2 / C5 graphs): wall vs library decode / h2d, per
+staging / mode variant (environment knobs of csrc/latbeam_b200.cu)."""
 import os
 import sys
 import time
@@ -14,8 +15,12 @@ g = synthetic.config_graph(name)
 d = synthetic.CONFIGS[name]["decode"]
 m = [np.ascontiguousarray(synthetic.config_matrix(name, 0).costs)]
 cfg = lb.DecodeConfig(beam=d["beam"], max_active=d["max_active"])
-for mode in ("batched", "lane", "batched"):
-    os.environ["LB_MODE"] = mode
+VARIANTS = {"auto": {}, "batched": {"LB_MODE": "batched"}, "copy": {"LB_E2E_COPY": "1"},
+            "noprog": {"LB_NO_PROGRESSIVE": "1"}}
+for mode in ("auto", "batched", "copy", "noprog", "auto"):
+    for k in ("LB_MODE", "LB_E2E_COPY", "LB_NO_PROGRESSIVE"):
+        os.environ.pop(k, None)
+    os.environ.update(VARIANTS[mode])
     lb.decode_batch(g, m, cfg, want_lattice=False)
     for _ in range(3):
         t0 = time.perf_counter()

@@ -7,6 +7,7 @@ import paper_1804_03243_b200 as lb
 from paper_1804_03243_b200 import synthetic
 
 os.environ["LB_MODE"] = "lane"
+os.environ["LB_ZC_MIN"] = "1"   # progressive zero-copy staging even for 2 utterances
 C = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 w = synthetic.hclg_graph(5, num_states=5000, pool_size=200, num_pdfs=50)
 ms = [synthetic.hclg_matrix(9 + i, num_frames=3, num_pdfs=50) for i in range(2)]
