@@ -48,7 +48,7 @@ typedef struct {
     int32_t collect_frame_packs;  /* keep per-frame token lists for readback */
     int32_t lanes;                /* concurrent utterances per launch (CTAs); 0 = auto */
     int32_t threads_per_lane;     /* CTA size: 512, 640 or 768; 0 = auto (640) */
-    int32_t ctas_per_lane;        /* thread-block cluster size of a lane (1..8); 0 = auto */
+    int32_t ctas_per_lane;        /* thread-block cluster size of a lane (1..16; >8 is a non-portable size); 0 = auto */
     int32_t keep_work_lattice;    /* also keep every live arc + extra (DecodeResult.work_lattice) */
 } lb_config;
 
