@@ -1503,7 +1503,8 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     if (!out) return set_err(LB_USAGE, "out is NULL");
     *out = nullptr;
     if (S < 1 || A < 0 || start < 0 || start >= S) return set_err(LB_USAGE, "bad graph dimensions / start state");
-    if (S >= (1ll << 31) || A >= (1ll << 32) - 1) return set_err(LB_USAGE, "graph too large for 32-bit ids");
+    if (S >= (1ll << 30) || A >= (1ll << 32) - 1)
+        return set_err(LB_USAGE, "graph too large: at most 2^30 - 1 states and 2^32 - 2 arcs");
     if (off[0] != 0 || off[S] != A) return set_err(LB_USAGE, "arc offsets must start at 0 and end at num_arcs");
     Nvtx range_("lb_graph_create");
     std::unique_ptr<lb_graph> g(new lb_graph());
@@ -1524,9 +1525,10 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     int *d_maxil = nullptr;
     unsigned long long *d_sum = nullptr;
     void *d_tmp = nullptr;
+    unsigned char *d_epsin = nullptr;
     auto cleanup = [&]() {
         cudaFree(d_off); cudaFree(d_dst); cudaFree(d_il); cudaFree(d_w); cudaFree(d_ecnt); cudaFree(d_emit);
-        cudaFree(d_err); cudaFree(d_maxil); cudaFree(d_sum); cudaFree(d_tmp);
+        cudaFree(d_err); cudaFree(d_maxil); cudaFree(d_sum); cudaFree(d_tmp); cudaFree(d_epsin);
     };
     struct Guard { std::function<void()> f; ~Guard() { f(); } } guard{cleanup};
     CK(dalloc(&d_off, S + 1));
@@ -1584,7 +1586,10 @@ int lb_graph_create(int32_t device, int64_t S, int64_t A, int32_t start, const i
     g->max_edeg = (int64_t)(unsigned)hsum[1];
     CK(dalloc(&g->eps, g->E));
     gb_state_eps<<<nb, 256, 0, st>>>(d_off, d_il, d_dst, d_w, S, g->eoff, g->eps, g->erng);
-    gb_arcs<<<nb, 256, 0, st>>>(d_dst, d_il, (const int *)g->ol, d_w, A, S, g->erng, g->arcs, d_err, d_maxil);
+    CK(dalloc(&d_epsin, S));
+    CK(cudaMemsetAsync(d_epsin, 0, S, st));
+    gb_eps_in<<<nb, 256, 0, st>>>(d_dst, d_il, A, S, d_epsin);
+    gb_arcs<<<nb, 256, 0, st>>>(d_dst, d_il, (const int *)g->ol, d_w, A, S, g->erng, d_epsin, g->arcs, d_err, d_maxil);
     CK(cudaGetLastError());
     int hmaxil = 0;
     CK(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));

@@ -42,6 +42,11 @@ enum : int {
 // per-state CSR of 16 B {dst, arc id, weight} records so the closure reads one
 // record per epsilon arc.
 constexpr unsigned EPS_FLAG = 0x80000000u;
+// arc record ilabel word / candidate state word: the destination has no incoming
+// epsilon arc, so no epsilon offer can change its word after emit (graphs of
+// < 2^30 states; lb_graph_create)
+constexpr unsigned NOEPSIN_FLAG = 0x40000000u;
+constexpr unsigned STATE_FLAGS = EPS_FLAG | NOEPSIN_FLAG;
 struct GraphDev {
     const int4 *arcs;
     const unsigned *src;
@@ -58,7 +63,7 @@ struct GraphDev {
     int _pad;
 };
 
-__device__ __forceinline__ unsigned arc_il(int y) { return (unsigned)y & ~EPS_FLAG; }
+__device__ __forceinline__ unsigned arc_il(int y) { return (unsigned)y & ~STATE_FLAGS; }
 
 // Per-state record of a lane: everything a touched state needs in ONE 32-byte
 // sector, laid out so each phase touches it with as few scattered accesses as

@@ -57,20 +57,29 @@ __global__ void gb_state_eps(const long long *off, const int *il, const int *dst
     }
 }
 
-// per arc: validation, the 16 B record with the "dst owns epsilon arcs" flag
+// states entered by an epsilon arc (ilabel 0)
+__global__ void gb_eps_in(const int *dst, const int *il, long long A, long long S, unsigned char *eps_in) {
+    for (long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x; a < A; a += (long long)gridDim.x * blockDim.x) {
+        const int d = dst[a];
+        if (il[a] == 0 && d >= 0 && d < S) eps_in[d] = 1;
+    }
+}
+
+// per arc: validation, the 16 B record with the "dst owns epsilon arcs" and
+// "dst has no incoming epsilon arc" flags
 __global__ void gb_arcs(const int *dst, const int *il, const int *ol, const double *w, long long A, long long S,
-                        const uint2 *erng, int4 *arcs, unsigned *err, int *max_il) {
+                        const uint2 *erng, const unsigned char *eps_in, int4 *arcs, unsigned *err, int *max_il) {
     int mx = 0;
     for (long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x; a < A; a += (long long)gridDim.x * blockDim.x) {
         const int d = dst[a], l = il[a];
-        if (d < 0 || d >= S || l < 0 || ol[a] < 0) {
+        if (d < 0 || d >= S || l < 0 || l >= (int)NOEPSIN_FLAG || ol[a] < 0) {
             atomicOr(err, GB_BAD_FIELD);
             continue;
         }
         const double x = w[a];
         if (!(x >= 0.0 && x <= 1.7976931348623157e308)) atomicOr(err, GB_BAD_WEIGHT);
         const uint2 er = erng[d];
-        const unsigned y = (unsigned)l | (er.y > er.x ? EPS_FLAG : 0u);
+        const unsigned y = (unsigned)l | (er.y > er.x ? EPS_FLAG : 0u) | (eps_in[d] ? 0u : NOEPSIN_FLAG);
         const long long bits = __double_as_longlong(x);
         arcs[a] = make_int4(d, (int)y, (int)(bits & 0xFFFFFFFFll), (int)(bits >> 32));
         mx = l > mx ? l : mx;

@@ -56,6 +56,7 @@ struct Smem {
     long long err_aux;
     // per CTA
     int ntouched[2], ncand[2], nseed[2], nfix[2], netouched[2];
+    int nfinal[2];                 // seeds final after winners (list B, top of the touched segment)
     int nfr[3];
     unsigned long long best[2];    // order-preserving f64 running best (frame parity)
     unsigned long long c_tok, c_scan, c_cand, c_front, c_escan, c_ecand, c_next;
@@ -397,6 +398,7 @@ struct Lane {
         if (G.leader()) G.M->ntok[q] = G.M->nlat[q] = 0;
         if (threadIdx.x == 0) {
             lane_sm.ntouched[q] = lane_sm.ncand[q] = lane_sm.nseed[q] = lane_sm.nfix[q] = lane_sm.netouched[q] = 0;
+            lane_sm.nfinal[q] = 0;
             lane_sm.best[q] = SENT;
         }
     }
@@ -494,7 +496,7 @@ struct Lane {
                 for (int u = 0; u < UNR; u++) {
                     if (em[u]) {
                         const long long bits = __double_as_longlong(cand[u]);
-                        const unsigned flag = (unsigned)r[u].y & EPS_FLAG;
+                        const unsigned flag = (unsigned)r[u].y & STATE_FLAGS;
                         const int k = cstart + cused + off[u];
                         CAND_ST(cb + k, make_int4((int)((unsigned)r[u].x | flag), (int)aa[u],
                                                  (int)(bits & 0xFFFFFFFFll), (int)(bits >> 32)));
@@ -560,18 +562,43 @@ struct Lane {
         double *c;
         int n;
     };
-    __device__ __forceinline__ void win_flush(WinStage &st, int *counter) const {
+    // Flush a winner stage: entries marked final (bit 31 of the state) go to list
+    // B, filled downward from the top of this CTA's touched segment (counter
+    // `nfin`); the others to list A from the bottom (counter `counter`).  The two
+    // never meet: together they hold at most one entry per candidate.
+    __device__ __forceinline__ void win_flush(WinStage &st, int *counter, int *nfin) const {
         __syncwarp();
         if (st.n == 0) return;
-        int base = 0;
-        if ((threadIdx.x & 31) == 0) base = atomicAdd(counter, st.n);
-        base = __shfl_sync(FULL, base, 0);
-        const size_t o = cseg() + base;
-        for (int i = threadIdx.x & 31; i < st.n; i += 32) {
-            PAY_ST(L.touched + o + i, st.v[i]);
-            PAY_ST(L.tarc + o + i, st.a[i]);
-            PAY_ST(L.tpred + o + i, st.p[i]);
-            PAY_ST(L.tcost + o + i, st.c[i]);
+        const int lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1u;
+        int nb = 0;
+        for (int i0 = 0; i0 < st.n; i0 += 32) {
+            const int i = i0 + lane;
+            nb += __popc(__ballot_sync(FULL, i < st.n && (st.v[i] >> 31)));
+        }
+        int ba = 0, bb = 0;
+        if (lane == 0) {
+            if (st.n > nb) ba = atomicAdd(counter, st.n - nb);
+            if (nb) bb = atomicAdd(nfin, nb);
+        }
+        ba = __shfl_sync(FULL, ba, 0);
+        bb = __shfl_sync(FULL, bb, 0);
+        const size_t cs = cseg(), top = cs + (size_t)L.ccap - 1;
+        for (int i0 = 0; i0 < st.n; i0 += 32) {
+            const int i = i0 + lane;
+            const bool in = i < st.n;
+            const unsigned v = in ? st.v[i] : 0u;
+            const bool fb = in && (v >> 31);
+            const unsigned mb = __ballot_sync(FULL, fb), ma = __ballot_sync(FULL, in && !fb);
+            if (in) {
+                const size_t o = fb ? top - (size_t)(bb + __popc(mb & lt)) : cs + (size_t)(ba + __popc(ma & lt));
+                PAY_ST(L.touched + o, v & 0x7FFFFFFFu);
+                PAY_ST(L.tarc + o, st.a[i]);
+                PAY_ST(L.tpred + o, st.p[i]);
+                PAY_ST(L.tcost + o, st.c[i]);
+            }
+            ba += __popc(ma);
+            bb += __popc(mb);
         }
         __syncwarp();
         st.n = 0;
@@ -642,7 +669,7 @@ struct Lane {
             cand_at(warp * 32 * WUNR + stride + u * 32 + lane, en[u], tn[u]);
         }
 #pragma unroll
-        for (int u = 0; u < WUNR; u++) pc[u] = ec[u].x != -1 ? rld_u64(pk + ((unsigned)ec[u].x & ~EPS_FLAG)) : 0ull;
+        for (int u = 0; u < WUNR; u++) pc[u] = ec[u].x != -1 ? rld_u64(pk + ((unsigned)ec[u].x & ~STATE_FLAGS)) : 0ull;
         for (int kb = warp * 32 * WUNR; kb < nc; kb += stride) {
             int4 e[WUNR];
             int ti[WUNR];
@@ -654,7 +681,7 @@ struct Lane {
                 pw[u] = pc[u];
                 ec[u] = en[u];
                 tc[u] = tn[u];
-                pc[u] = ec[u].x != -1 ? rld_u64(pk + ((unsigned)ec[u].x & ~EPS_FLAG)) : 0ull;
+                pc[u] = ec[u].x != -1 ? rld_u64(pk + ((unsigned)ec[u].x & ~STATE_FLAGS)) : 0ull;
                 cand_at(kb + 2 * stride + u * 32 + lane, en[u], tn[u]);
             }
 #else
@@ -688,11 +715,11 @@ struct Lane {
             unsigned long long pw[WUNR];
 #pragma unroll
             for (int u = 0; u < WUNR; u++)
-                pw[u] = e[u].x != -1 ? rld_u64(pk + ((unsigned)e[u].x & ~EPS_FLAG)) : 0ull;
+                pw[u] = e[u].x != -1 ? rld_u64(pk + ((unsigned)e[u].x & ~STATE_FLAGS)) : 0ull;
 #endif
 #pragma unroll
             for (int u = 0; u < WUNR; u++) {
-                const unsigned v = (unsigned)e[u].x & ~EPS_FLAG;
+                const unsigned v = (unsigned)e[u].x & ~STATE_FLAGS;
                 const double cand = __hiloint2double(e[u].w, e[u].z);
                 const bool own = e[u].x != -1 && pw[u] == pack_word(cand, (unsigned)e[u].y);
                 const bool seed = own && cand <= cutoff;
@@ -709,10 +736,20 @@ struct Lane {
 #else
                 const bool listed = own;
 #endif
+#ifndef LB_NO_FINAL_SEEDS
+                // A seed whose state has no incoming epsilon arc is final now: no
+                // epsilon offer can reach its word.  Reset the word here and list
+                // the seed in list B, which aggregate consumes without the atomic
+                // exchange (list A keeps the seeds epsilon offers may improve).
+                const bool fin = seed && ((unsigned)e[u].x & NOEPSIN_FLAG);
+                if (fin) rst_u64(pk + v, SENT);
+#else
+                const bool fin = false;
+#endif
                 const unsigned mo = __ballot_sync(FULL, listed);
                 if (listed) {
                     const int j = sw.n + __popc(mo & lt);
-                    sw.v[j] = v;
+                    sw.v[j] = v | (fin ? 0x80000000u : 0u);
                     sw.a[j] = (unsigned)e[u].y;
                     sw.p[j] = (ti[u] << 1) | 1;
                     sw.c[j] = cand;
@@ -729,11 +766,11 @@ struct Lane {
                 }
                 sf.n += __popc(mf);
                 if (hist && seed) atomicAdd(wh + hist_bin(cand, best, width, inv_w), 1);
-                if (sw.n > SWW - 32) win_flush(sw, ntouched);
+                if (sw.n > SWW - 32) win_flush(sw, ntouched, &lane_sm.nfinal[par]);
                 if (sf.n > SWW - 32) fr_flush(sf, nf0, f0);
             }
         }
-        win_flush(sw, ntouched);
+        win_flush(sw, ntouched, &lane_sm.nfinal[par]);
         fr_flush(sf, nf0, f0);
         nseed = warp_sum(nseed);
         if (lane == 0 && nseed) atomicAdd(&lane_sm.nseed[par], (int)nseed);
@@ -999,7 +1036,10 @@ struct Lane {
     }
 
     __device__ int aggregate(double cutoff, int frame, long long tb) {
-        const int nt = lane_sm.ntouched[par], ne = lane_sm.netouched[par], ntot = nt + ne;
+        // k in [0, nb): list B (final seeds, no exchange), [nb, nb + nt): list A,
+        // then the epsilon-reached states
+        const int nb = lane_sm.nfinal[par], nt = nb + lane_sm.ntouched[par];
+        const int ne = lane_sm.netouched[par], ntot = nt + ne;
         const long long room = io.tok_cap - tb;
         unsigned long long *pk = L.pk;
         const unsigned *tl = touched(), *etl = etouched();
@@ -1016,10 +1056,11 @@ struct Lane {
             pr = 0;
             c = 0.0;
             if (k < nt) {
-                v = PAY_LD(tl + k);
-                a = PAY_LD(L.tarc + cs + k);
-                pr = PAY_LD(L.tpred + cs + k);
-                c = PAY_LD(L.tcost + cs + k);
+                const size_t o = k < nb ? (size_t)L.ccap - 1 - (size_t)k : (size_t)(k - nb);
+                v = PAY_LD(tl + o);
+                a = PAY_LD(L.tarc + cs + o);
+                pr = PAY_LD(L.tpred + cs + o);
+                c = PAY_LD(L.tcost + cs + o);
             } else if (k < ntot) {
                 v = __ldcg(etl + (k - nt));
             }
@@ -1030,14 +1071,15 @@ struct Lane {
         fetch(warp * 32 + lane, vn, an, prn, cn);
         for (int kb = warp * 32; kb < ntot; kb += nw * 32) {
             const int k = kb + lane;
-            const bool valid = k < ntot, win = k < nt;
+            const bool valid = k < ntot, win = k < nt, fin = k < nb;
             unsigned v = vn, a = an;
             int pr = prn;
             double c = cn;
             fetch(k + nw * 32, vn, an, prn, cn);
             // read the final word and reset it in one atomic (issuing the next
-            // batch's exchanges a batch ahead measured no faster)
-            const unsigned long long x = valid ? atom_exch_u64(pk + v, SENT) : SENT;
+            // batch's exchanges a batch ahead measured no faster); a final seed's
+            // word is its own and was reset in winners
+            const unsigned long long x = fin ? pack_word(c, a) : valid ? atom_exch_u64(pk + v, SENT) : SENT;
             if (valid && (!win || x != pack_word(c, a))) {   // improved by an epsilon offer
                 const ulonglong2 er = rld_u128(L.erec + v);
                 c = __longlong_as_double((long long)er.x);
@@ -1138,11 +1180,12 @@ struct Lane {
     // ---- error path: O(touched) reset of every per-state word this frame touched ----
     __device__ void reset_touched() {
         G.sync();
-        const int nt = lane_sm.ntouched[par], ne = lane_sm.netouched[par];
+        const int nb = lane_sm.nfinal[par], nt = lane_sm.ntouched[par], ne = lane_sm.netouched[par];
         const unsigned *tl = touched(), *etl = etouched();
         const double inf = inf_d();
-        for (int k = threadIdx.x; k < nt + ne; k += blockDim.x) {
-            const unsigned v = k < nt ? __ldcg(tl + k) : __ldcg(etl + (k - nt));
+        for (int k = threadIdx.x; k < nb + nt + ne; k += blockDim.x) {
+            const unsigned v = k < nb ? __ldcg(tl + L.ccap - 1 - k)
+                             : k < nb + nt ? __ldcg(tl + (k - nb)) : __ldcg(etl + (k - nb - nt));
             rst_u64(L.pk + v, SENT);
             rst_f64(L.msnap + v, inf);
             rst_u128(rpk(0) + v, make_ulonglong2(~0ull, ~0ull));
@@ -1158,6 +1201,7 @@ __device__ __forceinline__ void init_smem(unsigned round_ctr) {
         for (int q = 0; q < 2; q++) {
             sm.ntok[q] = sm.nlat[q] = 0;
             sm.ntouched[q] = sm.ncand[q] = sm.nseed[q] = sm.nfix[q] = sm.netouched[q] = 0;
+            sm.nfinal[q] = 0;
             sm.best[q] = SENT;
         }
         sm.nfr[0] = sm.nfr[1] = sm.nfr[2] = 0;
@@ -1780,14 +1824,16 @@ expand_kernel(const __grid_constant__ GraphDev g, const __grid_constant__ Params
     __syncthreads();
     // the closure's states: emitting winners / seeds with their payload, then the
     // epsilon-reached ones; the final word says whether epsilon improved a state
-    const int nt = sm.ntouched[1], ne = sm.netouched[1];
+    // (list B first: final seeds whose words winners already reset)
+    const int nb = sm.nfinal[1], nt = nb + sm.ntouched[1], ne = sm.netouched[1];
     const unsigned *tl = ln.touched(), *etl = ln.etouched();
     for (int k = tid; k < nt + ne; k += blockDim.x) {
-        const bool win = k < nt;
-        const unsigned v = win ? __ldcg(tl + k) : __ldcg(etl + (k - nt));
-        double c = win ? __ldcg(L.tcost + k) : 0.0;
-        const unsigned a = win ? __ldcg(L.tarc + k) : 0u;
-        const unsigned long long x = atom_exch_u64(L.pk + v, SENT);
+        const bool win = k < nt, fin = k < nb;
+        const size_t o = fin ? (size_t)L.ccap - 1 - (size_t)k : (size_t)(k - nb);
+        const unsigned v = win ? __ldcg(tl + o) : __ldcg(etl + (k - nt));
+        double c = win ? __ldcg(L.tcost + o) : 0.0;
+        const unsigned a = win ? __ldcg(L.tarc + o) : 0u;
+        const unsigned long long x = fin ? pack_word(c, a) : atom_exch_u64(L.pk + v, SENT);
         if (!win || x != pack_word(c, a)) c = __ldcg(&L.erec[v].cost);
         if (c <= cutoff) {
             const int idx = agg_append(&sm.ntok[1]);

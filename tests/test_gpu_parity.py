@@ -74,10 +74,11 @@ def test_lane_cta_sizes(oracle_mod, monkeypatch, threads):
         check_pair(got, ref, 3.0)
 
 
-@pytest.mark.parametrize("ctas", [3, 4, 8])
+@pytest.mark.parametrize("ctas", [3, 4, 8, 16])
 def test_wide_lane_clusters(oracle_mod, monkeypatch, ctas):
-    """3-, 4- and 8-CTA lane clusters (picked automatically for 5-45 utterance
-    1-best batches) decode 1-best and lattices bit-exactly vs the oracle."""
+    """3-, 4-, 8- and 16-CTA lane clusters (picked automatically for batches of up
+    to 45 utterances; 16 CTAs is a non-portable cluster size) decode 1-best and
+    lattices bit-exactly vs the oracle."""
     monkeypatch.setenv("LB_MODE", "lane")
     rng = np.random.default_rng(ctas)
     for seed in range(14_000_000, 14_000_020):
@@ -88,10 +89,11 @@ def test_wide_lane_clusters(oracle_mod, monkeypatch, ctas):
         check_pair(got, ref, 3.0)
 
 
-@pytest.mark.parametrize("n", [3, 8, 20, 40])
+@pytest.mark.parametrize("n", [1, 3, 8, 20, 40])
 def test_auto_mode_batches(oracle_mod, n):
-    """The automatic mode choice (batched at 3, 8-CTA lanes at 8, 4-CTA lanes at
-    20, 3-CTA lanes at 40 utterances) gives the oracle's costs and work counters."""
+    """The automatic mode choice (16-CTA lanes at 1 and 3, 8-CTA lanes at 8, 4-CTA
+    lanes at 20, 3-CTA lanes at 40 utterances) gives the oracle's costs and work
+    counters."""
     w = synthetic.hclg_graph(4, num_states=300_000, pool_size=4000, num_pdfs=500)
     mats = [synthetic.hclg_matrix(700 + i, num_frames=30 + (i % 7), num_pdfs=500) for i in range(n)]
     cfg = lb.DecodeConfig(beam=12.0, max_active=2000)
