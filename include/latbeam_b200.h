@@ -57,7 +57,9 @@ const char *lb_last_error(void);
 int32_t lb_device_count(void);
 
 /* Wfst (wfst.py:33-90): CSR columns, arc id = position.  Uploaded to HBM on
- * `device` as 16 B arc records + side columns. */
+ * `device` as 16 B arc records + side columns.  Limits: fewer
+ * than 2^30 states, 2^32 - 1 arcs and input labels below 2^30 (two flag bits
+ * ride in the state and label words); LB_USAGE otherwise. */
 int lb_graph_create(int32_t device, int64_t num_states, int64_t num_arcs, int32_t start_state,
                     const int64_t *arc_offsets, const int32_t *arc_src, const int32_t *arc_dst,
                     const int32_t *arc_ilabel, const int32_t *arc_olabel, const double *arc_weight,
