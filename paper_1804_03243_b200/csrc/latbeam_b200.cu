@@ -1106,7 +1106,8 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
     for (int u = 0; u < n && aligned && !ring; u++) aligned = ((uintptr_t)dev_costs[u] & 15) == 0;
     p.row_pf = !batched && p.acrow_smem && !d_ready && !costs_f32 && (D % 2 == 0) && aligned &&
                !getenv("LB_NO_ROWPF") && lane_dyn_smem(threads, D, true, true) <= 227 * 1024;
-    const size_t smem = lane_dyn_smem(threads, D, p.acrow_smem != 0, p.row_pf != 0);
+    size_t smem = lane_dyn_smem(threads, D, p.acrow_smem != 0, p.row_pf != 0);
+    if (const char *e = getenv("LB_SMEM_PAD")) smem += (size_t)atoi(e);   // measurement knob (L1 carveout)
     // decode-lane variants: CTA size x batch width x lattice x phase-profile
     using KernT = void (*)(const GraphDev, const Params, const LaneWs *, const UttDesc *, const UttJob *, int, int *);
     const bool prof = p.prof != nullptr;

@@ -145,10 +145,10 @@ constexpr int WMAP = 512;
 #define PAY_ST __stcg
 #define PAY_LD __ldcg
 #endif
-template <int UNR, class F>
+template <int UNR, class OwnT, class F>
 __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, int gwarp, int gnw,
                                                            const unsigned *ts, const double *tc, int n,
-                                                           unsigned &c_scan, int *own, F &&f) {
+                                                           unsigned &c_scan, OwnT *own, F &&f) {
     const int lane = threadIdx.x & 31;
     const int step = gnw * 32;
     int base = gwarp * 32;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void for_each_token_arc_batched(const GraphDev &g, in
         if (lane == 0) c_scan += (unsigned)total;
         const bool mapped = total <= WMAP;
         if (mapped) {
-            for (int j = excl; j < incl; j++) own[j] = lane;
+            for (int j = excl; j < incl; j++) own[j] = (OwnT)lane;
             __syncwarp();
         }
         for (int j0 = 0; j0 < total; j0 += 32 * UNR) {
@@ -230,7 +230,7 @@ static_assert(SWW * 20 + SWW * 12 <= WSCR, "winners stages fit the warp scratch"
 // `row_pf`: two row buffers (the next frame's row is prefetched, Lane::row_async).
 inline size_t lane_dyn_smem(int threads, int D, bool acrow_smem, bool row_pf = false) {
     const size_t nw = (size_t)threads / 32;
-    return (acrow_smem ? (size_t)D * 8 * (row_pf ? 2 : 1) : 0) + nw * WMAP * 4 + nw * WSCR + nw * NBINS * 4;
+    return (acrow_smem ? (size_t)D * 8 * (row_pf ? 2 : 1) : 0) + nw * WMAP + nw * WSCR + nw * NBINS * 4;
 }
 constexpr int CAND_CHUNK = 256;   // Lane::CCH
 
@@ -270,16 +270,18 @@ struct Lane {
     const double *row;      // global row of the current frame
     int par;                // parity of the current frame (counter set)
 
-    // Dynamic shared memory (lane_dyn): [acrow: D f64 when p.acrow_smem][owner maps]
-    // [per-warp scratch][per-warp histograms].  Addresses are derived from the
+    // Dynamic shared memory (lane_dyn): [acrow: D f64 when p.acrow_smem][per-warp
+    // scratch][per-warp histograms][byte owner maps].  Addresses are derived from the
     // namespace-scope shared array at each use so they stay shared::cta.
     __device__ Lane(const GraphDev &g_, const Params &p_, const LaneWs &L_, const UttDesc &io_,
                     const Grp &G_, double *)
         : g(g_), p(p_), L(L_), io(io_), G(G_), row(nullptr), par(0) {}
     __device__ __forceinline__ int acrow_doubles() const { return p.acrow_smem ? p.D * (p.row_pf ? 2 : 1) : 0; }
-    __device__ __forceinline__ int *own_all() const { return reinterpret_cast<int *>(lane_dyn + acrow_doubles()); }
-    __device__ __forceinline__ char *scratch_all() const {
-        return reinterpret_cast<char *>(own_all() + (blockDim.x >> 5) * WMAP);
+    // [acrow][per-warp scratch][per-warp histograms][byte owner maps]: a lane id
+    // fits a byte, and every byte of shared memory saved is L1 capacity
+    __device__ __forceinline__ char *scratch_all() const { return reinterpret_cast<char *>(lane_dyn + acrow_doubles()); }
+    __device__ __forceinline__ unsigned char *own_all() const {
+        return reinterpret_cast<unsigned char *>(scratch_all() + (blockDim.x >> 5) * (WSCR + NBINS * 4));
     }
     __device__ __forceinline__ int *whist_all() const {
         return reinterpret_cast<int *>(scratch_all() + (blockDim.x >> 5) * WSCR);
@@ -317,7 +319,7 @@ struct Lane {
     __device__ __forceinline__ EpsWin *rpk(int r) const { return L.rpk + (size_t)(r & 1) * L.S; }
 
     __device__ __forceinline__ unsigned *fixes() const { return L.fix + (size_t)G.rank * L.S; }
-    __device__ __forceinline__ int *wmap() const { return own_all() + (threadIdx.x >> 5) * WMAP; }
+    __device__ __forceinline__ unsigned char *wmap() const { return own_all() + (threadIdx.x >> 5) * WMAP; }
 
     __device__ __forceinline__ double ac(unsigned il) const {
         // with the row prefetch, frame t's row (t-1) sits in buffer (t-1)&1 = par^1
