@@ -280,7 +280,7 @@ int ensure_workspace(lb_graph *g, Workspace &w, int lanes, int C, int64_t ccap, 
     // Reallocate to exactly this request (never the max of old and new: the
     // lane budget in decode_impl was computed for this request alone).
     w.release();
-    ccap = std::max<int64_t>(ccap, 1);
+    ccap = (std::max<int64_t>(ccap, 1) + 31) & ~(int64_t)31;   // 128-byte lines per 32-entry batch (discard)
     const size_t S = (size_t)g->S, nl = (size_t)lanes, nc = (size_t)C;
     auto A = [&](auto **p, size_t n) -> cudaError_t {
         cudaError_t e = dalloc(p, n);

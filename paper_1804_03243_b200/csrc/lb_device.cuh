@@ -205,13 +205,21 @@ struct __align__(16) EpsWin {
 // Per-lane scratch.  O(S) arrays are allocated once and reset
 // O(touched) per frame.  Lists marked [C] have one S-sized segment per CTA of
 // the lane (CTA-local append counters in shared memory, no DSMEM traffic).
-// candidate buffer cache policy: streamed (evict-first) by default
-#ifdef LB_CAND_CG
-#define CAND_ST __stcg
-#define CAND_LD __ldcg
-#else
+// Candidate buffer cache policy: L2-normal stores and loads.  winners() reads
+// each 32-entry batch once and then drops its lines from L2 with
+// discard.global.L2 (LB_CAND_DISCARD, the default), so the buffer lives and dies
+// in L2 without a DRAM write-back (C4 539k -> 555k frames/s,
+// profiles/r02_ab_discard.txt; evict-first stores without the discard were the
+// round-1 policy, LB_CAND_CS).
+#ifdef LB_CAND_CS
 #define CAND_ST __stcs
 #define CAND_LD __ldcs
+#else
+#define CAND_ST __stcg
+#define CAND_LD __ldcg
+#endif
+#if !defined(LB_NO_CAND_DISCARD) && !defined(LB_CAND_CS)
+#define LB_CAND_DISCARD 1
 #endif
 
 // Epsilon-improved state: its final f64 cost and predecessor (source state << 1).

@@ -771,6 +771,15 @@ struct Lane {
                 if (sw.n > SWW - 32) win_flush(sw, ntouched, &lane_sm.nfinal[par]);
                 if (sf.n > SWW - 32) fr_flush(sf, nf0, f0);
             }
+#ifdef LB_CAND_DISCARD
+            // this batch's candidate lines are dead (read once, their values are in
+            // registers and used above): drop them from L2 without a write-back
+            if (lane < 5 * WUNR) {
+                const int q = lane % 5, uu = lane / 5;
+                const void *a = q < 4 ? (const void *)(cb + kb + uu * 32 + q * 8) : (const void *)(cbi + kb + uu * 32);
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+            }
+#endif
         }
         win_flush(sw, ntouched, &lane_sm.nfinal[par]);
         fr_flush(sf, nf0, f0);
