@@ -241,6 +241,12 @@ struct lb_graph {
     size_t ring_cap = 0;
     int *ring_ctl = nullptr;  // [0] ready count, [32..] per-slot done marks (mapped pinned)
     int ring_ctl_cap = 0;
+    double *dring = nullptr;  // device copy of the ring (DMA staging, decode_ring)
+    size_t dring_cap = 0;
+    int *dring_ready = nullptr;   // device ready count, written by the copy stream
+    int *ring_seq = nullptr;      // pinned sequence values 1..n the copy stream writes into dring_ready
+    int ring_seq_cap = 0;
+    cudaStream_t copy_stream = nullptr;
     GraphDev dev() const {
         GraphDev g;
         g.arcs = arcs;
@@ -1358,12 +1364,18 @@ int decode_impl(lb_graph *g, int32_t n, const double *const *dev_costs, const in
 }
 
 // Streamed host input for a refilling decode: job k (LPT queue order) is copied
-// into slot k % R of a mapped pinned ring by host threads and published in
-// order through a mapped counter (Params::ring_ready); a lane that finishes job
-// j hands its slot back (ring_done[slot] = j + 1) and the host reuses it for
-// job j + R.  Host memory stays bounded (R slots) and the copy overlaps the
+// into slot k % R of a pinned ring by host threads; a lane that finishes job j
+// hands its slot back (ring_done[slot] = j + 1, mapped) and the host reuses it
+// for job j + R.  Host memory stays bounded (R slots) and the copy overlaps the
 // decode instead of preceding it (pinned buffering of the
 // log-likelihood H2D).
+//  * DMA ring (default): a publisher thread enqueues, in queue order, the H2D
+//    copy of slot k into the same slot of a device ring and then a 4-byte copy
+//    of k + 1 into a device ready counter (Params::ring_ready), both on one copy
+//    stream, so the counter passes k only after job k's rows are in HBM.  The
+//    lanes read their rows from HBM, exactly as an HBM-resident decode does.
+//  * Zero-copy ring (LB_RING_ZC=1): the ring is mapped and the lanes read the
+//    rows over PCIe; the ready counter is mapped and published by the stagers.
 int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T, int D, const lb_config *cfg,
                 int lanes, lb_result *res) {
     Nvtx range_("lb.decode_ring");
@@ -1387,13 +1399,40 @@ int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T
         CK(cudaHostAlloc((void **)&g->ring_ctl, sizeof(int) * (size_t)(R + 32), cudaHostAllocMapped));
         g->ring_ctl_cap = R + 32;
     }
+    const bool dma = !getenv("LB_RING_ZC");
+    if (dma) {
+        if (need > g->dring_cap) {
+            if (g->dring) cudaFree(g->dring);
+            g->dring = nullptr;
+            g->dring_cap = 0;
+            CK(cudaMalloc((void **)&g->dring, need));
+            g->dring_cap = need;
+        }
+        if (!g->dring_ready) CK(cudaMalloc((void **)&g->dring_ready, 128));
+        if (n + 1 > g->ring_seq_cap) {
+            if (g->ring_seq) cudaFreeHost(g->ring_seq);
+            g->ring_seq = nullptr;
+            g->ring_seq_cap = 0;
+            CK(cudaHostAlloc((void **)&g->ring_seq, sizeof(int) * (size_t)(n + 1), cudaHostAllocDefault));
+            g->ring_seq_cap = n + 1;
+            for (int k = 0; k <= n; k++) g->ring_seq[k] = k;
+        }
+        if (!g->copy_stream) CK(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+        CK(cudaMemsetAsync(g->dring_ready, 0, sizeof(int), g->copy_stream));
+        CK(cudaStreamSynchronize(g->copy_stream));   // zero before the kernel can read it
+    }
     int *h_ready = g->ring_ctl, *h_done = g->ring_ctl + 32;   // ready on its own line
     __atomic_store_n(h_ready, 0, __ATOMIC_SEQ_CST);
     for (int k = 0; k < R; k++) __atomic_store_n(h_done + k, 0, __ATOMIC_SEQ_CST);
     RingDev rd;
-    CK(cudaHostGetDevicePointer((void **)&rd.ready, h_ready, 0));
+    if (dma) {
+        rd.ready = g->dring_ready;
+        rd.base = g->dring;
+    } else {
+        CK(cudaHostGetDevicePointer((void **)&rd.ready, h_ready, 0));
+        CK(cudaHostGetDevicePointer((void **)&rd.base, g->ring, 0));
+    }
     CK(cudaHostGetDevicePointer((void **)&rd.done, h_done, 0));
-    CK(cudaHostGetDevicePointer((void **)&rd.base, g->ring, 0));
     rd.slot_doubles = slot_doubles;
     rd.slots = R;
     const std::vector<int32_t> ord = lpt_order(n, T);
@@ -1406,6 +1445,7 @@ int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T
     std::atomic<bool> abort_flag{false};
     char *ring = reinterpret_cast<char *>(g->ring);
     auto publish = [&]() {   // advance the in-order published count as far as staged jobs allow
+        if (dma) return;         // (the publisher thread below does it)
         int r = pub.load(std::memory_order_acquire);
         while (r < n && staged[r].load(std::memory_order_acquire)) {
             if (pub.compare_exchange_weak(r, r + 1, std::memory_order_acq_rel)) {
@@ -1432,15 +1472,40 @@ int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T
             publish();
         }
     };
+    // DMA publisher: job k's slot copy, then the counter, in queue order
+    std::atomic<int> dma_err{0};
+    auto publisher = [&]() {
+        cudaSetDevice(g->device);
+        for (int k = 0; k < n; k++) {
+            int spins = 0;
+            while (!staged[k].load(std::memory_order_acquire)) {
+                if (abort_flag.load(std::memory_order_relaxed)) return;
+                if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(10));
+            }
+            const size_t off = (size_t)(k % R) * slot_doubles;
+            cudaError_t e = cudaMemcpyAsync(g->dring + off, g->ring + off, (size_t)T[ord[k]] * D * 8,
+                                            cudaMemcpyHostToDevice, g->copy_stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(g->dring_ready, g->ring_seq + k + 1, sizeof(int), cudaMemcpyHostToDevice,
+                                    g->copy_stream);
+            if (e != cudaSuccess) {
+                dma_err.store((int)e);
+                return;
+            }
+        }
+    };
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nth; t++) th.emplace_back(work, t);
+    if (dma) th.emplace_back(publisher);
     const int rc = decode_impl(g, n, costs, T, D, cfg, g->stream, res, 0.0f, nullptr, &rd);
     // a kernel that ran to the end consumed every job, so the stagers are done;
     // after a failure they may wait on a slot that is never handed back
     abort_flag.store(true);
     for (auto &x : th) x.join();
+    if (dma) CK(cudaStreamSynchronize(g->copy_stream));
     res->t_h2d = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == LB_OK && dma_err.load()) return set_err(LB_CUDA, cudaGetErrorString((cudaError_t)dma_err.load()));
     return rc;
 }
 
@@ -1627,6 +1692,10 @@ int lb_graph_destroy(lb_graph *g) {
     if (g->h_ready) cudaFreeHost(g->h_ready);
     if (g->ring) cudaFreeHost(g->ring);
     if (g->ring_ctl) cudaFreeHost(g->ring_ctl);
+    if (g->dring) cudaFree(g->dring);
+    if (g->dring_ready) cudaFree(g->dring_ready);
+    if (g->ring_seq) cudaFreeHost(g->ring_seq);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
     if (g->stream) cudaStreamDestroy(g->stream);
     if (g->stream2) cudaStreamDestroy(g->stream2);
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);

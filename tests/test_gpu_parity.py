@@ -462,14 +462,18 @@ def _ragged_batch(n, seed0, num_pdfs=300, tmin=8, tmax=70):
                                                        num_pdfs=num_pdfs).costs) for i in range(n)]
 
 
-@pytest.mark.parametrize("slots", [0, 1, 3])
-def test_refilling_lanes_streamed_ring(oracle_mod, monkeypatch, slots):
+@pytest.mark.parametrize("slots,zc", [(0, False), (1, False), (3, False), (0, True), (3, True)])
+def test_refilling_lanes_streamed_ring(oracle_mod, monkeypatch, slots, zc):
     """A ragged batch much larger than the lane count: one launch, lanes refill
     from the longest-first job queue, host rows stream through the pinned ring
     (LB_RING_SLOTS forces heavy slot reuse: every slot is rewritten many times
-    inside one kernel).  Every utterance equals the oracle, in input order."""
+    inside one kernel), copied slot by slot into a device ring on a copy stream
+    (default) or read zero-copy over PCIe (LB_RING_ZC).  Every utterance equals
+    the oracle, in input order."""
     if slots:
         monkeypatch.setenv("LB_RING_SLOTS", str(slots))
+    if zc:
+        monkeypatch.setenv("LB_RING_ZC", "1")
     w = synthetic.hclg_graph(9, num_states=60_000, pool_size=1500, num_pdfs=300)
     mats = _ragged_batch(90, 7000 + slots)
     cfg = lb.DecodeConfig(beam=12.0, max_active=600, lanes=6)
