@@ -22,7 +22,8 @@ mats = [torch.from_numpy(np.array(synthetic.hclg_matrix(100 + i, num_frames=T).c
         for i in range(U)]
 names = ("tok", "scan", "cand", "efront", "escan", "ecand", "next", "lat")
 for ctas, thr in confs:
-    cfg = lb.DecodeConfig(beam=13.0, max_active=7000, ctas_per_lane=ctas, threads_per_lane=thr, lanes=U)
+    cfg = lb.DecodeConfig(beam=13.0, max_active=7000, ctas_per_lane=ctas, threads_per_lane=thr,
+                          lanes=int(os.environ.get("LB_PHASE_LANES", U)))
     decode_batch_resident(g, mats, cfg)
     outs, tm = decode_batch_resident(g, mats, cfg)
     per = {k: v / U / T * 1e3 for k, v in tm["phases_ms"].items()}
