@@ -18,6 +18,7 @@
 #include <string>
 #include <atomic>
 #include <thread>
+#include <sys/mman.h>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX 3: ranges are free unless a profiler injects itself
@@ -2167,6 +2168,18 @@ int lb_result_final_arrays(const lb_result *r, int32_t utt, uint64_t *node_keys,
     return LB_OK;
 }
 
+// Ask for transparent huge pages on a fresh destination array before it is
+// first touched: the widening below is page-fault bound on new numpy memory
+// (4 KB faults), and 2 MB pages cut the fault count 512x.  Only the 2 MB-aligned
+// interior is advised; a no-op where THP is off (LB_NO_THP disables it).
+static void hugepage_hint(void *p, size_t bytes) {
+    static const bool off = getenv("LB_NO_THP") != nullptr;
+    if (off || !p || bytes < ((size_t)4 << 20)) return;
+    const uintptr_t a = ((uintptr_t)p + ((1u << 21) - 1)) & ~(uintptr_t)((1u << 21) - 1);
+    const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((1u << 21) - 1);
+    if (e > a) madvise((void *)a, e - a, MADV_HUGEPAGE);
+}
+
 int lb_result_final_arrays64(const lb_result *r, int32_t utt, int64_t *node_frame, int64_t *node_idx,
                              int64_t *final_ids, double *final_costs, int64_t *from, int64_t *to, int64_t *ilabel,
                              int64_t *olabel, double *graph_cost, double *acoustic_cost) {
@@ -2177,6 +2190,11 @@ int lb_result_final_arrays64(const lb_result *r, int32_t utt, int64_t *node_fram
     if (final_costs) std::memcpy(final_costs, u.fl_final_costs.data(), 8 * nf);
     // widen from the pinned arena on all host threads (the copies are page-fault
     // bound on fresh numpy pages, which parallelise)
+    for (int64_t *q : {from, to, ilabel, olabel}) hugepage_hint(q, 8 * m);
+    hugepage_hint(graph_cost, 8 * m);
+    hugepage_hint(acoustic_cost, 8 * m);
+    hugepage_hint(node_frame, 8 * nn);
+    hugepage_hint(node_idx, 8 * nn);
     unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     if (m + nn < ((size_t)1 << 18)) nth = 1;
     auto work = [&](unsigned w) {
