@@ -1490,7 +1490,15 @@ int decode_ring(lb_graph *g, int n, const double *const *costs, const int32_t *T
                 e = cudaMemcpyAsync(g->dring_ready, g->ring_seq + k + 1, sizeof(int), cudaMemcpyHostToDevice,
                                     g->copy_stream);
             if (e != cudaSuccess) {
+                // release the lanes (they would wait for job k forever): publish
+                // every job from a fresh stream; the call then fails with LB_CUDA
                 dma_err.store((int)e);
+                cudaStream_t rs = nullptr;
+                if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) == cudaSuccess) {
+                    cudaMemcpyAsync(g->dring_ready, g->ring_seq + n, sizeof(int), cudaMemcpyHostToDevice, rs);
+                    cudaStreamSynchronize(rs);
+                    cudaStreamDestroy(rs);
+                }
                 return;
             }
         }
